@@ -1,0 +1,194 @@
+/*
+ * l1pcp_b200 — C ABI of the B200-native l1-filtering PCP hot path.
+ *
+ * This is the drop-in boundary for the data-parallel core of the reference package
+ * `l1pcp` (/root/reference/pkg/src/l1pcp). The reference is pure Python/numpy and has no
+ * FFI of its own, so each entry point below names the reference function it replaces
+ * (file:line, relative to pkg/src/l1pcp/); a reference-side binding (ctypes) is shown in
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless the parameter name ends in `_host`.
+ *  - Matrices are row-major with an explicit leading dimension (elements, not bytes).
+ *  - "Unit-major" panels store one l1-regression unit (a column of the reference's X,
+ *    l1reg.py:59) contiguously: x_u[i] = X[u*ldx + i].
+ *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and is
+ *    stream-ordered; entry points that return host values synchronise that stream.
+ *  - Return value: L1F_OK (0) or a negative L1F_ERR_* code; l1f_last_error() gives the
+ *    message for the calling thread. No exception crosses the ABI.
+ *  - dtype codes: L1F_F32 (float) / L1F_F64 (double).
+ */
+#ifndef L1PCP_B200_H_
+#define L1PCP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define L1F_OK 0
+#define L1F_ERR_ARG (-1)          /* invalid argument (reference: ValueError)              */
+#define L1F_ERR_CUDA (-2)         /* CUDA runtime failure                                   */
+#define L1F_ERR_SVD (-3)          /* SVD did not converge (matcore.py:9-10,82-85)           */
+#define L1F_ERR_DIVERGED (-4)     /* non-finite PCP residual (pcp_adm.py:19-20,126-129)     */
+#define L1F_ERR_UNSUPPORTED (-5)  /* shape outside the compiled kernel family               */
+
+#define L1F_F32 0
+#define L1F_F64 1
+
+/* per-unit status written by l1f_filter_* (reference bookkeeping l1reg.py:107-135) */
+#define L1F_UNIT_OK 0       /* res <= tol*||x||_inf                                        */
+#define L1F_UNIT_STALLED 1  /* 20 iterations of relative change < 1e-12, not ok -> failed   */
+#define L1F_UNIT_MAXITER 2  /* max_iter exhausted -> failed                                 */
+#define L1F_UNIT_ZERO 3     /* ||x||_inf == 0: z = e = 0, iterations 0, not failed          */
+
+/* generator kinds for l1f_generate_f32 */
+#define L1F_GEN_GAUSSIAN 0  /* L0 = X Y^T, X,Y ~ N(0,1); S0 Bernoulli(rho_s) x U[-mag,mag]  */
+#define L1F_GEN_VIDEO 1     /* L0 = X Y^T, X ~ U[0,1), Y ~ U[0,1)*255/r; S0 moving boxes    */
+
+const char* l1f_last_error(void);
+int l1f_version(void);
+/* number of SMs of the current device, written to *out_host */
+int l1f_sm_count(int* out_host);
+
+/* ------------------------------------------------------------------------------------
+ * Column-separable l1 regression by ADM — replaces `_solve_block` (l1reg.py:59-137), the
+ * body of `solve_l1reg` (l1reg.py:140-160) and `solve_l1reg_columnwise`
+ * (l1reg.py:163-214).  Solves, independently per unit u (x_u of length s):
+ *     min ||e||_1  s.t.  x_u = A z_u + e_u,   A (s x k) with orthonormal columns,
+ * with the reference's per-unit penalty schedule (beta0 = 1/||x_u||_inf unless beta0>0;
+ * beta_max = 1e7*beta0 unless beta_max>0), per-unit stop res <= tol*||x_u||_inf,
+ * stagnation rule (20 iterations below 1e-12 relative change) and max_iter.
+ *  X   unit-major panel, n_units x s, leading dimension ldx >= s
+ *  A   s x k row-major (lda >= k); orthonormality is validated by the caller
+ *  Z   unit-major output n_units x k (ldz >= k)            -> reference z (transposed)
+ *  E   unit-major output n_units x s (lde >= s), nullable  -> reference e (transposed)
+ *  iters/res/status: per-unit iteration count, final max|r|, L1F_UNIT_* code (nullable)
+ *  workspace: l1f_filter_workspace_bytes() bytes, or NULL to allocate stream-ordered.
+ * Results are bitwise independent of n_units, unit order and GPU count.
+ * ---------------------------------------------------------------------------------- */
+size_t l1f_filter_workspace_bytes(int dtype, int32_t s, int32_t k, int64_t n_units);
+int l1f_filter_f32(const float* X, int64_t ldx, int32_t s, int64_t n_units,
+                   const float* A, int64_t lda, int32_t k,
+                   float tol, float rho, float beta0, float beta_max, int32_t max_iter,
+                   float* Z, int64_t ldz, float* E, int64_t lde,
+                   int32_t* iters, float* res, uint8_t* status,
+                   void* workspace, size_t workspace_bytes, void* stream);
+int l1f_filter_f64(const double* X, int64_t ldx, int32_t s, int64_t n_units,
+                   const double* A, int64_t lda, int32_t k,
+                   double tol, double rho, double beta0, double beta_max, int32_t max_iter,
+                   double* Z, int64_t ldz, double* E, int64_t lde,
+                   int32_t* iters, double* res, uint8_t* status,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Index gather — replaces `m[np.ix_(rows, cols)]` (l1filter.py:87 sample_submatrix,
+ * :242-243 panel extraction).  out[r][c] = M[rows[r]][cols[c]] (transpose=0) or
+ * out[c][r] (transpose=1, the unit-major column panel).  rows/cols may be NULL (= arange).
+ * Converts dtype_in -> dtype_out on the fly.
+ * ---------------------------------------------------------------------------------- */
+int l1f_gather(int dtype_in, const void* M, int64_t ldm,
+               const int64_t* rows, int64_t n_rows, const int64_t* cols, int64_t n_cols,
+               int dtype_out, void* out, int64_t ldo, int32_t transpose, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Rank-k completion factors — the unified form of `nystrom_complete` (l1filter.py:137-141)
+ * and the four blocks of `assemble` (l1filter.py:151-167):  L[i][j] = Af[i] . Bf[j] with
+ *   Af[i] = U[p]                 (i = row_idx[p], a seed row)
+ *         = Zr[i'] / sigma       (i the i'-th non-seed row; Zr = P~^T, unit-major)
+ *   Bf[j] = sigma * V[q]         (j = col_idx[q], a seed column)
+ *         = Zc[j']               (j the j'-th non-seed column; Zc = Q~^T, unit-major)
+ * row_idx / col_idx must be sorted ascending (sample_submatrix sorts them, l1filter.py:85-86).
+ * U (s_r x k), sigma (k), V (s_c x k) are the seed factors in FP64.
+ * ---------------------------------------------------------------------------------- */
+int l1f_build_factors(int dtype, int64_t m, int64_t n, int32_t k,
+                      const int64_t* row_idx, int64_t s_r, const int64_t* col_idx, int64_t s_c,
+                      const double* U, const double* sigma, const double* V,
+                      const void* Zc, int64_t ldzc, const void* Zr, int64_t ldzr,
+                      void* Af, void* Bf, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Reconstruction + residual — replaces `nystrom_complete`+`assemble` (l1filter.py:137-167),
+ * `s = m - l` (:253) and the residual numerator/denominator (:256-257):
+ *   L = Af Bf^T (m x n, K = k),  S = M - L,  resid_sq[0] += sum((M-L)-S)^2,
+ *   resid_sq[1] += sum(M^2)   (resid_sq is a device double[2], zeroed by the callee).
+ * M and S may be NULL (then only L is formed, e.g. the completion block alone).
+ * ---------------------------------------------------------------------------------- */
+int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k,
+                    const void* Af, int64_t ldaf, const void* Bf, int64_t ldbf,
+                    const void* M, int64_t ldm, void* L, int64_t ldl, void* S, int64_t lds,
+                    double* resid_sq, void* stream);
+
+/* General C = alpha * A B^T (+ beta*C), A m x k, B n x k, row-major; used for the small
+ * dense products of the reference API (SkinnySvd.reconstruct matcore.py:36-38,
+ * pseudo_inverse_apply matcore.py:116-123, nystrom_complete_via_pinv l1filter.py:144-148). */
+int l1f_gemm_nt(int dtype, int64_t m, int64_t n, int64_t k, double alpha,
+                const void* A, int64_t lda, const void* B, int64_t ldb,
+                double beta, void* C, int64_t ldc, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Synthetic inputs — replaces `synth.generate` (synth.py:43-64) for the benchmark configs
+ * by a counter-based Philox4x64-10 generator (bit-identical to numpy.random.Philox with
+ * counter = block index), so any row shard [row0, row0+rows) is reproducible on any rank.
+ *  l1f_generate_factors_f32: X (m x r) and Y (n x r) row-major.
+ *  l1f_generate_f32: rows [row0,row0+rows) of M = L0 + S0 (and of L0 when L0 != NULL),
+ *     L0[i][j] = sum_t X[i][t]*Y[j][t] accumulated in t order with separately rounded
+ *     multiply and add (no FMA), so the numpy oracle reproduces it bit for bit.
+ * ---------------------------------------------------------------------------------- */
+int l1f_generate_factors_f32(uint64_t seed, int32_t kind, int64_t m, int64_t n, int32_t r,
+                             float* X, float* Y, void* stream);
+int l1f_generate_f32(uint64_t seed, int32_t kind, int64_t m, int64_t n, int32_t r,
+                     float rho_s, float magnitude, const float* X, const float* Y,
+                     int64_t row0, int64_t rows, float* M, int64_t ldm,
+                     float* L0, int64_t ldl0, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Reductions — `frobenius_norm`, `l1_norm`, `linf_norm`, `l0_count` and the finiteness
+ * check of `as_dense` (matcore.py:13-20,41-63).  out (device double[5]):
+ *   [0] sum|x|, [1] max|x|, [2] sum x^2, [3] count(|x| > thr), [4] count(non-finite)
+ * Deterministic (fixed-order two-level reduction, no float atomics).
+ * l1f_diff_norms: out2 = { sum (a-b)^2, sum b^2 }  (rel_err synth.py:92-97)
+ * ---------------------------------------------------------------------------------- */
+int l1f_norms(int dtype, const void* X, int64_t rows, int64_t cols, int64_t ld, double thr,
+              double* out5, void* stream);
+int l1f_diff_norms(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb,
+                   int64_t rows, int64_t cols, double* out2, void* stream);
+/* Y = sign(X) * max(|X| - eta, 0) elementwise (matcore.py:66-70); X, Y may alias. */
+int l1f_soft_threshold(int dtype, const void* X, void* Y, int64_t count, double eta,
+                       void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Seed-stage dense kernels (FP64) — the small PCP of `recover_seed` (l1filter.py:90-113).
+ *  l1f_svd_f64: thin SVD W = U diag(sigma) V^T, p = min(m,n), sigma descending
+ *     (matcore.py:73-88 before the rank cut).  U m x p, V n x p, row-major.
+ *  l1f_spectral_norm_f64: 25-step power iteration from the all-ones vector
+ *     (pcp_adm.py:69-87); result to *out_host.
+ *  l1f_svt_f64: out = U max(sigma - eta, 0) V^T and *rank_host = #(sigma > eta)
+ *     (matcore.py:96-105).
+ *  l1f_pcp_f64: inexact-ALM PCP (pcp_adm.py:90-140) with lam, beta0 (<=0: 1.25/||M||_2),
+ *     beta_max (<=0: 1e7*beta0), rho, tol, max_iter.  Host outputs: iterations, final
+ *     residual, rank of L, converged flag, final beta.
+ * ---------------------------------------------------------------------------------- */
+int l1f_svd_f64(const double* W, int64_t m, int64_t n, int64_t ldw,
+                double* U, double* sigma, double* V, void* stream);
+int l1f_spectral_norm_f64(const double* M, int64_t m, int64_t n, int32_t iters,
+                          double* out_host, void* stream);
+int l1f_svt_f64(const double* W, int64_t m, int64_t n, double eta, double* out,
+                int32_t* rank_host, void* stream);
+int l1f_pcp_f64(const double* M, int64_t m, int64_t n, double lam, double tol,
+                double beta0, double rho, double beta_max, int32_t max_iter,
+                double* L, double* S, int32_t* iters_host, double* residual_host,
+                int32_t* rank_host, int32_t* converged_host, double* beta_final_host,
+                void* stream);
+
+/* FP32 FMA-throughput microbenchmark (roofline denominator for the filter kernel):
+ * runs `iters` dependent-chain FMA loops on every SM; *flops_host = FLOPs executed. */
+int l1f_fma_peak_probe(int32_t iters, float* sink, double* flops_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* L1PCP_B200_H_ */

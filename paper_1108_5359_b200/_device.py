@@ -1,0 +1,101 @@
+"""Device plumbing: torch tensors for memory and streams, the C-ABI for all compute.
+
+Type policy of the drop-in API (mirrors the reference's numpy-in/numpy-out contract):
+  * numpy / array-like inputs are coerced like ``as_dense`` (float64) and the results come
+    back as new float64 numpy arrays;
+  * torch CUDA tensors stay on the device (float32 is kept as float32 — the benchmark
+    path — anything else becomes float64) and results are torch tensors.
+"""
+
+import numpy as np
+
+from . import _lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+def require_cuda():
+    """Fail loudly when there is no GPU or no native library; there is no CPU fallback."""
+    if torch is None or not torch.cuda.is_available():
+        raise _lib.NativeUnavailable("a CUDA device is required: l1pcp_b200 has no CPU path")
+    _lib.load()
+
+
+def is_tensor(a):
+    return torch is not None and isinstance(a, torch.Tensor)
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dtype_code(t):
+    return _lib.F32 if t.dtype == torch.float32 else _lib.F64
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def as_device(a, keep_f32=True):
+    """Return (contiguous CUDA tensor, came_from_host)."""
+    require_cuda()
+    if is_tensor(a):
+        t = a
+        if t.dtype not in (torch.float32, torch.float64) or (t.dtype == torch.float32 and not keep_f32):
+            t = t.to(torch.float64)
+        if not t.is_cuda:
+            t = t.cuda()
+        return t.contiguous(), False
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return torch.from_numpy(arr).cuda(), True
+
+
+def to_host_if(t, host):
+    if not host:
+        return t
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def empty(shape, dtype=None, like=None):
+    dt = dtype if dtype is not None else (like.dtype if like is not None else torch.float64)
+    return torch.empty(shape, dtype=dt, device="cuda")
+
+
+def zeros(shape, dtype=None, like=None):
+    dt = dtype if dtype is not None else (like.dtype if like is not None else torch.float64)
+    return torch.zeros(shape, dtype=dt, device="cuda")
+
+
+def transpose(t):
+    """Materialised transpose through the C-ABI gather kernel (out[c][r] = t[r][c])."""
+    r, c = t.shape
+    out = empty((c, r), like=t)
+    code = dtype_code(t)
+    _lib.call("l1f_gather", code, ptr(t), t.stride(0), None, r, None, c, code, ptr(out), r, 1, stream())
+    return out
+
+
+def norms(t, thr=0.0):
+    """(sum|x|, max|x|, sum x^2, count(|x|>thr), count(non-finite)) on the device."""
+    t = t.contiguous()
+    out = zeros(5, dtype=torch.float64)
+    rows = t.shape[0] if t.dim() == 2 else 1
+    cols = t.shape[1] if t.dim() == 2 else t.numel()
+    _lib.call("l1f_norms", dtype_code(t), ptr(t), rows, cols, cols, float(thr), ptr(out), stream())
+    return out.cpu().tolist()
+
+
+def gemm_nt(a, b, alpha=1.0, k=None, out=None, beta=0.0):
+    """alpha * a[:, :k] @ b[:, :k].T (+ beta * out) with the C-ABI tile GEMM."""
+    m, n = a.shape[0], b.shape[0]
+    kk = a.shape[1] if k is None else k
+    if out is None:
+        out = empty((m, n), like=a)
+        beta = 0.0
+    _lib.call("l1f_gemm_nt", dtype_code(a), m, n, kk, float(alpha), ptr(a), a.stride(0), ptr(b), b.stride(0),
+              float(beta), ptr(out), out.stride(0), stream())
+    return out

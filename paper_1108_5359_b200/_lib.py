@@ -1,0 +1,162 @@
+"""ctypes binding of the C-ABI library ``libl1pcp_b200.so`` (declared in include/l1pcp_b200.h).
+
+The library is built in-tree (``paper_1108_5359_b200/_lib/``) by ``__graft_entry__.build()``
+or ``make -C paper_1108_5359_b200/csrc``.  There is no fallback: if the library or a CUDA
+device is missing, every compute entry point raises :class:`NativeUnavailable`.
+"""
+
+import ctypes
+import glob
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libl1pcp_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "l1pcp_b200.h")
+
+L1F_OK = 0
+L1F_ERR_ARG = -1
+L1F_ERR_CUDA = -2
+L1F_ERR_SVD = -3
+L1F_ERR_DIVERGED = -4
+L1F_ERR_UNSUPPORTED = -5
+
+F32 = 0
+F64 = 1
+
+UNIT_OK, UNIT_STALLED, UNIT_MAXITER, UNIT_ZERO = 0, 1, 2, 3
+GEN_GAUSSIAN, GEN_VIDEO = 0, 1
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension (or a CUDA device) is not available; there is no CPU fallback."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned an error status."""
+
+    def __init__(self, code, message):
+        super().__init__(message)
+        self.code = code
+
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_f32 = ctypes.c_float
+_f64 = ctypes.c_double
+_sz = ctypes.c_size_t
+_int = ctypes.c_int
+
+# name -> (restype, argtypes); mirrors include/l1pcp_b200.h
+SIGNATURES = {
+    "l1f_last_error": (ctypes.c_char_p, []),
+    "l1f_version": (_int, []),
+    "l1f_sm_count": (_int, [_vp]),
+    "l1f_filter_workspace_bytes": (_sz, [_int, _i32, _i32, _i64]),
+    "l1f_filter_f32": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _i32,
+                              _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "l1f_filter_f64": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f64, _f64, _f64, _f64, _i32,
+                              _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "l1f_gather": (_int, [_int, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp, _i64, _i32, _vp]),
+    "l1f_build_factors": (_int, [_int, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
+                                 _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "l1f_reconstruct": (_int, [_int, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                               _vp, _i64, _vp, _vp]),
+    "l1f_gemm_nt": (_int, [_int, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _vp]),
+    "l1f_generate_factors_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "l1f_generate_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _f32, _f32, _vp, _vp, _i64, _i64,
+                                _vp, _i64, _vp, _i64, _vp]),
+    "l1f_norms": (_int, [_int, _vp, _i64, _i64, _i64, _f64, _vp, _vp]),
+    "l1f_diff_norms": (_int, [_int, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "l1f_soft_threshold": (_int, [_int, _vp, _vp, _i64, _f64, _vp]),
+    "l1f_svd_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "l1f_spectral_norm_f64": (_int, [_vp, _i64, _i64, _i32, _vp, _vp]),
+    "l1f_svt_f64": (_int, [_vp, _i64, _i64, _f64, _vp, _vp, _vp]),
+    "l1f_pcp_f64": (_int, [_vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp,
+                           _vp, _vp, _vp, _vp]),
+    "l1f_fma_peak_probe": (_int, [_i32, _vp, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _preload_cuda_libraries():
+    """Make the CUDA math libraries resolve to the copies torch already uses.
+
+    torch ships its own cuBLAS/cuSOLVER; loading those (RTLD_GLOBAL) before our library
+    keeps one consistent set in the process.  Outside a torch environment the library's
+    RPATH (/usr/local/cuda/lib64) is used instead.
+    """
+    try:
+        import nvidia  # noqa: F401  (namespace package of the CUDA wheels)
+    except ImportError:
+        return
+    roots = [os.path.dirname(p) for p in getattr(__import__("nvidia"), "__path__", [])]
+    for sub, names in (("cublas", ("libcublasLt.so.*", "libcublas.so.*")),
+                       ("cusolver", ("libcusolver.so.*",))):
+        for root in roots:
+            for pat in names:
+                for path in sorted(glob.glob(os.path.join(root, "nvidia", sub, "lib", pat))):
+                    try:
+                        ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+                    except OSError:
+                        pass
+
+
+def load(path=None):
+    """Load (once) and return the ctypes handle of the C-ABI library."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise NativeUnavailable(
+                f"{p} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "or `make -C paper_1108_5359_b200/csrc`")
+        try:
+            import torch  # noqa: F401  (loads torch's CUDA libraries first)
+        except ImportError:
+            pass
+        _preload_cuda_libraries()
+        lib = ctypes.CDLL(p, mode=ctypes.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def last_error():
+    return load().l1f_last_error().decode(errors="replace")
+
+
+def check(code, what=""):
+    """Raise the reference's exception type for a non-zero status."""
+    if code == L1F_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if code == L1F_ERR_ARG:
+        raise ValueError(msg)
+    if code == L1F_ERR_SVD:
+        from .matcore import SvdConvergenceError
+        raise SvdConvergenceError(msg)
+    if code == L1F_ERR_DIVERGED:
+        from .pcp_adm import PcpDivergenceError
+        raise PcpDivergenceError(msg)
+    raise NativeError(code, msg)
+
+
+def call(name, *args, what=None):
+    code = getattr(load(), name)(*args)
+    check(code, what or name)
+    return code

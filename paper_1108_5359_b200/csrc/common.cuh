@@ -1,0 +1,83 @@
+// Shared helpers for the l1-filtering PCP kernels (sm_100a).
+//
+// Every C-ABI entry point returns an int status (L1F_OK or a negative code) and
+// records a human-readable message retrievable through l1f_last_error(); no C++
+// exception crosses the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <float.h>
+#include <string>
+
+#include "../../include/l1pcp_b200.h"
+
+namespace l1f {
+
+void set_error(const char* fmt, ...);
+
+#define L1F_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ::l1f::set_error("%s:%d: %s: %s", __FILE__, __LINE__, #expr,                \
+                       cudaGetErrorString(_e));                                   \
+      return L1F_ERR_CUDA;                                                        \
+    }                                                                             \
+  } while (0)
+
+#define L1F_CHECK_LAUNCH() L1F_CUDA_TRY(cudaGetLastError())
+
+#define L1F_REQUIRE(cond, code, ...)                                              \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      ::l1f::set_error(__VA_ARGS__);                                              \
+      return (code);                                                              \
+    }                                                                             \
+  } while (0)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms();
+
+template <typename T> struct Limits;
+template <> struct Limits<float> {
+  __host__ __device__ static constexpr float tiny() { return FLT_MIN; }
+  __host__ __device__ static constexpr float inf() { return __builtin_huge_valf(); }
+};
+template <> struct Limits<double> {
+  __host__ __device__ static constexpr double tiny() { return DBL_MIN; }
+  __host__ __device__ static constexpr double inf() { return __builtin_huge_val(); }
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float  tabs(float v)  { return fabsf(v); }
+__device__ __forceinline__ double tabs(double v) { return fabs(v); }
+__device__ __forceinline__ float  tmax(float a, float b)   { return fmaxf(a, b); }
+__device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
+
+// sign(w) * max(|w| - t, 0), the reference's soft threshold
+// (pkg/src/l1pcp/matcore.py:66-70; per-unit use at l1reg.py:97).
+template <typename T>
+__device__ __forceinline__ T shrink(T w, T t) {
+  T m = tabs(w) - t;
+  m = m > T(0) ? m : T(0);
+  return w > T(0) ? m : (w < T(0) ? -m : T(0));
+}
+
+}  // namespace l1f

@@ -1,0 +1,362 @@
+// FP64 seed stage of l1 filtering: the small PCP of recover_seed (l1filter.py:90-113).
+//
+//   solve_pcp          pcp_adm.py:90-140   (inexact ALM: shrink, SVT, residual, dual/penalty)
+//   spectral_norm_est. pcp_adm.py:69-87    (25-step power iteration from the all-ones vector)
+//   svd / svt_with_rank matcore.py:73-105  (thin SVD; singular value thresholding)
+//
+// The SVD itself is cuSOLVER's gesvd (a library factorisation, run once per ALM
+// iteration on the s x s seed); everything around it — the fused shrink/residual/dual
+// kernels, the deterministic reductions and the rank-k SVT product — is ours.  The seed
+// runs in FP64: its factors must pass the reference's orthonormality check
+// (l1reg.py:48-56, 1e-8) before they are cast to FP32 for the filter.
+#include "common.cuh"
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <vector>
+
+namespace l1f {
+namespace seed {
+
+struct Handles {
+  cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
+};
+
+static int handles(cudaStream_t st, Handles*& out) {
+  static thread_local Handles h;
+  if (!h.sol) {
+    if (cusolverDnCreate(&h.sol) != CUSOLVER_STATUS_SUCCESS) {
+      set_error("cusolverDnCreate failed");
+      return L1F_ERR_CUDA;
+    }
+  }
+  if (!h.blas) {
+    if (cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS) {
+      set_error("cublasCreate failed");
+      return L1F_ERR_CUDA;
+    }
+  }
+  cusolverDnSetStream(h.sol, st);
+  cublasSetStream(h.blas, st);
+  out = &h;
+  return L1F_OK;
+}
+
+struct Buf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Buf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 16, s); }
+  double* d() const { return (double*)p; }
+  ~Buf() { if (p) cudaFreeAsync(p, s); }
+};
+
+// S = shrink((M - L) + Y/b, lam/b) ; W = (M - S) + Y/b        (pcp_adm.py:122-123)
+__global__ void pcp_shrink_kernel(const double* __restrict__ M, const double* __restrict__ L,
+                                  const double* __restrict__ Y, double* __restrict__ S, double* __restrict__ W,
+                                  int64_t count, double beta, double thr) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const double yb = Y[e] / beta;
+    const double s = shrink((M[e] - L[e]) + yb, thr);
+    S[e] = s;
+    W[e] = (M[e] - s) + yb;
+  }
+}
+
+// R = (M - L) - S ; partial sum R^2 ; Y += b R                 (pcp_adm.py:124-130)
+__global__ void pcp_residual_kernel(const double* __restrict__ M, const double* __restrict__ L,
+                                    const double* __restrict__ S, double* __restrict__ Y, int64_t count,
+                                    double beta, double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const double r = (M[e] - L[e]) - S[e];
+    acc += r * r;
+    Y[e] = Y[e] + beta * r;
+  }
+  __shared__ double red[32];
+  acc = warp_sum(acc);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += red[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += part[i];
+    *out = t;
+  }
+}
+
+// sum of squares, deterministic
+__global__ void sumsq_partial_kernel(const double* __restrict__ X, int64_t count, double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+    acc += X[e] * X[e];
+  __shared__ double red[32];
+  acc = warp_sum(acc);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += red[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+// U[:, t] *= w[t] for t < k (row-major m x ld)
+__global__ void scale_cols_kernel(double* __restrict__ U, int64_t m, int64_t ld, int k, const double* __restrict__ w) {
+  const int64_t total = m * (int64_t)k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k;
+    const int t = (int)(e - i * k);
+    U[i * ld + t] *= w[t];
+  }
+}
+
+static int reduce_blocks() { return num_sms() * 2; }
+
+static int sumsq(const double* X, int64_t count, double* part, double* out_dev, double* out_host, cudaStream_t st) {
+  const int g = reduce_blocks();
+  sumsq_partial_kernel<<<g, 256, 0, st>>>(X, count, part);
+  L1F_CHECK_LAUNCH();
+  sum_kernel<<<1, 32, 0, st>>>(part, g, out_dev);
+  L1F_CHECK_LAUNCH();
+  L1F_CUDA_TRY(cudaMemcpyAsync(out_host, out_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  return L1F_OK;
+}
+
+// Thin SVD of a row-major m x n matrix.  Row-major W is column-major W^T; cuSOLVER's gesvd
+// needs rows >= cols, so the n >= m case factors W^T in place and the n < m case factors
+// an explicit column-major copy of W.
+static int svd_rowmajor(Handles* h, const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sig,
+                        double* V, cudaStream_t st) {
+  const int64_t p = m < n ? m : n;
+  const bool wide = n >= m;  // factor A = W^T (n x m, col-major)
+  const int R = (int)(wide ? n : m), C = (int)(wide ? m : n);
+  Buf a(st), ucm(st), vtcm(st), work(st), info(st);
+  L1F_CUDA_TRY(a.alloc(sizeof(double) * (size_t)R * C));
+  const double one = 1.0, zero = 0.0;
+  if (wide) {
+    // column-major R x C with ld R: A(j, i) = W[i][j]  -> W rows are A columns
+    cublasDgeam(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, R, C, &one, W, (int)ldw, &zero, W, (int)ldw, a.d(), R);
+  } else {
+    // column-major m x n = transpose of the (n x m col-major) view of W
+    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, R, C, &one, W, (int)ldw, &zero, W, (int)ldw, a.d(), R);
+  }
+  L1F_CUDA_TRY(ucm.alloc(sizeof(double) * (size_t)R * p));
+  L1F_CUDA_TRY(vtcm.alloc(sizeof(double) * (size_t)p * C));
+  int lwork = 0;
+  if (cusolverDnDgesvd_bufferSize(h->sol, R, C, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("gesvd_bufferSize failed");
+    return L1F_ERR_CUDA;
+  }
+  L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
+  L1F_CUDA_TRY(info.alloc(sizeof(int)));
+  cusolverStatus_t cs = cusolverDnDgesvd(h->sol, 'S', 'S', R, C, a.d(), R, sig, ucm.d(), R, vtcm.d(), (int)p,
+                                         work.d(), lwork, nullptr, (int*)info.p);
+  if (cs != CUSOLVER_STATUS_SUCCESS) {
+    set_error("cusolverDnDgesvd failed with status %d", (int)cs);
+    return L1F_ERR_SVD;
+  }
+  int info_h = 0;
+  L1F_CUDA_TRY(cudaMemcpyAsync(&info_h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  if (info_h != 0) {
+    set_error("SVD failed on (%lld, %lld) matrix: gesvd info %d", (long long)m, (long long)n, info_h);
+    return L1F_ERR_SVD;
+  }
+  if (wide) {
+    // left vectors of W^T are V (n x p col-major) ; VT^T = U (p x m col-major == m x p row-major)
+    L1F_CUDA_TRY(cudaMemcpyAsync(U, vtcm.p, sizeof(double) * (size_t)p * C, cudaMemcpyDeviceToDevice, st));
+    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, R, &one, ucm.d(), R, &zero, ucm.d(), R, V, (int)p);
+  } else {
+    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, R, &one, ucm.d(), R, &zero, ucm.d(), R, U, (int)p);
+    L1F_CUDA_TRY(cudaMemcpyAsync(V, vtcm.p, sizeof(double) * (size_t)p * C, cudaMemcpyDeviceToDevice, st));
+  }
+  L1F_CHECK_LAUNCH();
+  return L1F_OK;
+}
+
+// out = U diag(max(sig - eta, 0)) V^T for the leading k with sig > eta  (matcore.py:96-105)
+static int svt_into(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
+                    cudaStream_t st) {
+  const int64_t p = m < n ? m : n;
+  Buf u(st), v(st), sg(st);
+  L1F_CUDA_TRY(u.alloc(sizeof(double) * (size_t)m * p));
+  L1F_CUDA_TRY(v.alloc(sizeof(double) * (size_t)n * p));
+  L1F_CUDA_TRY(sg.alloc(sizeof(double) * (size_t)p));
+  int rc = svd_rowmajor(h, W, m, n, n, u.d(), sg.d(), v.d(), st);
+  if (rc) return rc;
+  std::vector<double> sh((size_t)p);
+  L1F_CUDA_TRY(cudaMemcpyAsync(sh.data(), sg.p, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  // svd(w, rank_tol=0) keeps sigma > 0; then s = sigma - eta, k = #(s > 0)
+  int k = 0;
+  for (int64_t t = 0; t < p; ++t) {
+    if (!(sh[(size_t)t] > 0.0)) break;
+    const double sv = sh[(size_t)t] - eta;
+    if (sv > 0.0) { sh[(size_t)t] = sv; ++k; } else break;
+  }
+  *rank = k;
+  if (k == 0) {
+    L1F_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)m * n, st));
+    return L1F_OK;
+  }
+  L1F_CUDA_TRY(cudaMemcpyAsync(sg.p, sh.data(), sizeof(double) * (size_t)k, cudaMemcpyHostToDevice, st));
+  scale_cols_kernel<<<num_sms() * 4, 256, 0, st>>>(u.d(), m, p, k, sg.d());
+  L1F_CHECK_LAUNCH();
+  rc = l1f_gemm_nt(L1F_F64, m, n, k, 1.0, u.p, p, v.p, p, 0.0, out, n, st);
+  if (rc) return rc;
+  // keep the host vector alive until the H2D copy has been consumed
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  return L1F_OK;
+}
+
+static int spectral_norm(Handles* h, const double* M, int64_t m, int64_t n, int iters, double* out, cudaStream_t st) {
+  // row-major M (m x n) == column-major A = M^T (n x m, ld n)
+  Buf v(st), w(st);
+  L1F_CUDA_TRY(v.alloc(sizeof(double) * (size_t)n));
+  L1F_CUDA_TRY(w.alloc(sizeof(double) * (size_t)m));
+  std::vector<double> ones((size_t)n, 1.0 / std::sqrt((double)n));
+  L1F_CUDA_TRY(cudaMemcpyAsync(v.p, ones.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, st));
+  cublasSetPointerMode(h->blas, CUBLAS_POINTER_MODE_HOST);
+  const double one = 1.0, zero = 0.0;
+  double sigma = 0.0;
+  for (int i = 0; i < iters; ++i) {
+    double nw = 0.0;
+    cublasDgemv(h->blas, CUBLAS_OP_T, (int)n, (int)m, &one, M, (int)n, v.d(), 1, &zero, w.d(), 1);  // w = M v
+    cublasDnrm2(h->blas, (int)m, w.d(), 1, &nw);
+    if (nw == 0.0) { *out = 0.0; return L1F_OK; }
+    const double inv = 1.0 / nw;
+    cublasDscal(h->blas, (int)m, &inv, w.d(), 1);
+    cublasDgemv(h->blas, CUBLAS_OP_N, (int)n, (int)m, &one, M, (int)n, w.d(), 1, &zero, v.d(), 1);  // v = M^T w
+    cublasDnrm2(h->blas, (int)n, v.d(), 1, &sigma);
+    if (sigma == 0.0) { *out = 0.0; return L1F_OK; }
+    const double is = 1.0 / sigma;
+    cublasDscal(h->blas, (int)n, &is, v.d(), 1);
+  }
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  *out = sigma;
+  return L1F_OK;
+}
+
+}  // namespace seed
+}  // namespace l1f
+
+using namespace l1f;
+using namespace l1f::seed;
+
+extern "C" int l1f_svd_f64(const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sigma, double* V,
+                           void* stream) {
+  L1F_REQUIRE(m >= 1 && n >= 1 && ldw >= n, L1F_ERR_ARG, "svd: bad shape");
+  L1F_REQUIRE(m < INT32_MAX && n < INT32_MAX, L1F_ERR_UNSUPPORTED, "svd: matrix too large");
+  Handles* h;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  return svd_rowmajor(h, W, m, n, ldw, U, sigma, V, st);
+}
+
+extern "C" int l1f_spectral_norm_f64(const double* M, int64_t m, int64_t n, int32_t iters, double* out_host,
+                                     void* stream) {
+  L1F_REQUIRE(m >= 1 && n >= 1 && iters >= 0, L1F_ERR_ARG, "spectral_norm: bad shape");
+  Handles* h;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  return spectral_norm(h, M, m, n, iters, out_host, st);
+}
+
+extern "C" int l1f_svt_f64(const double* W, int64_t m, int64_t n, double eta, double* out, int32_t* rank_host,
+                           void* stream) {
+  L1F_REQUIRE(m >= 1 && n >= 1, L1F_ERR_ARG, "svt: bad shape");
+  L1F_REQUIRE(eta >= 0.0, L1F_ERR_ARG, "eta must be nonnegative");
+  Handles* h;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  int k = 0;
+  rc = svt_into(h, W, m, n, eta, out, &k, st);
+  *rank_host = k;
+  return rc;
+}
+
+extern "C" int l1f_pcp_f64(const double* M, int64_t m, int64_t n, double lam, double tol, double beta0, double rho,
+                           double beta_max, int32_t max_iter, double* L, double* S, int32_t* iters_host,
+                           double* residual_host, int32_t* rank_host, int32_t* converged_host,
+                           double* beta_final_host, void* stream) {
+  L1F_REQUIRE(m >= 1 && n >= 1, L1F_ERR_ARG, "matrix must be nonempty");
+  L1F_REQUIRE(rho > 1.0 && tol > 0.0 && lam > 0.0, L1F_ERR_ARG, "pcp: need rho > 1, tol > 0, lam > 0");
+  Handles* h;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  const int64_t count = m * n;
+  const int g = reduce_blocks();
+  Buf y(st), w(st), part(st), scal(st);
+  L1F_CUDA_TRY(part.alloc(sizeof(double) * (size_t)g));
+  L1F_CUDA_TRY(scal.alloc(sizeof(double)));
+  double norm2 = 0.0;
+  rc = sumsq(M, count, part.d(), scal.d(), &norm2, st);
+  if (rc) return rc;
+  const double norm_m = std::sqrt(norm2);
+  L1F_CUDA_TRY(cudaMemsetAsync(L, 0, sizeof(double) * (size_t)count, st));
+  L1F_CUDA_TRY(cudaMemsetAsync(S, 0, sizeof(double) * (size_t)count, st));
+  *iters_host = 0; *residual_host = 1.0; *rank_host = 0; *converged_host = 0; *beta_final_host = 0.0;
+  if (norm_m == 0.0) {  // pcp_adm.py:99-105
+    *iters_host = 1; *residual_host = 0.0; *converged_host = 1;
+    L1F_CUDA_TRY(cudaStreamSynchronize(st));
+    return L1F_OK;
+  }
+  double beta = beta0;
+  if (!(beta0 > 0.0)) {
+    double sn = 0.0;
+    rc = spectral_norm(h, M, m, n, 25, &sn, st);
+    if (rc) return rc;
+    beta = 1.25 / (sn > DBL_MIN ? sn : DBL_MIN);
+  }
+  const double bmax = beta_max > 0.0 ? beta_max : 1e7 * beta;
+  L1F_CUDA_TRY(y.alloc(sizeof(double) * (size_t)count));
+  L1F_CUDA_TRY(w.alloc(sizeof(double) * (size_t)count));
+  L1F_CUDA_TRY(cudaMemsetAsync(y.p, 0, sizeof(double) * (size_t)count, st));
+  double residual = 1.0;
+  int rank = 0, it = 0, converged = 0;
+  const int eg = num_sms() * 8;
+  for (it = 1; it <= max_iter; ++it) {
+    pcp_shrink_kernel<<<eg, 256, 0, st>>>(M, L, y.d(), S, w.d(), count, beta, lam / beta);
+    L1F_CHECK_LAUNCH();
+    rc = svt_into(h, w.d(), m, n, 1.0 / beta, L, &rank, st);
+    if (rc) return rc;
+    pcp_residual_kernel<<<g, 256, 0, st>>>(M, L, S, y.d(), count, beta, part.d());
+    L1F_CHECK_LAUNCH();
+    sum_kernel<<<1, 32, 0, st>>>(part.d(), g, scal.d());
+    L1F_CHECK_LAUNCH();
+    double r2 = 0.0;
+    L1F_CUDA_TRY(cudaMemcpyAsync(&r2, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    L1F_CUDA_TRY(cudaStreamSynchronize(st));
+    residual = std::sqrt(r2) / norm_m;
+    if (!std::isfinite(residual)) {
+      set_error("non-finite residual at iteration %d (beta=%.3g)", it, beta);
+      return L1F_ERR_DIVERGED;
+    }
+    if (residual <= tol) { converged = 1; break; }
+    beta = std::min(rho * beta, bmax);
+  }
+  if (it > max_iter) it = max_iter;
+  *iters_host = it;
+  *residual_host = residual;
+  *rank_host = rank;
+  *converged_host = converged;
+  *beta_final_host = beta;
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  return L1F_OK;
+}

@@ -1,0 +1,316 @@
+"""Device-resident l1-filtering pipeline: seed stage, filter stage, reconstruction.
+
+This is the engine behind ``estimate_rank_and_solve`` (l1filter.py:174-268) and the
+benchmark.  All matrices are CUDA tensors; every arithmetic step is a C-ABI kernel:
+
+  seed stage      host index sampling (numpy SeedSequence/Generator, identical to the
+                  reference so index sets match bit for bit) -> device gather ->
+                  l1f_pcp_f64 -> l1f_svd_f64 -> rank cut at rank_tol * sigma_max
+  filter stage    unit-major panel gathers -> l1f_filter_* for the column units (against
+                  U^s) and the row units (against V^s)
+  reconstruction  l1f_build_factors -> l1f_reconstruct (L = Af Bf^T, S = M - L, residual)
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dv
+from . import _lib
+from .pcp_adm import AdmConfig, default_lambda, solve_pcp_device
+
+torch = dv.torch
+
+
+class SeedRankZeroError(RuntimeError):
+    """The recovered seed matrix is (numerically) zero (l1filter.py:30-31)."""
+
+
+@dataclass
+class DeviceSeed:
+    row_idx: np.ndarray      # sorted int64 (host)
+    col_idx: np.ndarray
+    u: object                # (s_r, k) float64 CUDA
+    sigma: object            # (k,)
+    v: object                # (s_c, k)
+    seed_l: object           # (s_r, s_c) float64 CUDA, truncated reconstruction
+    block: object            # (s_r, s_c) float64 CUDA
+    r_prime: int
+    pcp_iterations: int
+
+
+def sample_indices(m_rows, m_cols, n_rows, n_cols, rng_seed):
+    """Index sets of sample_submatrix (l1filter.py:73-87): uniform without replacement,
+    sorted.  Host numpy RNG on purpose: it keeps the reference's index sets exactly."""
+    if n_rows > m_rows or n_cols > m_cols:
+        raise ValueError(f"requested {n_rows}x{n_cols} block from {m_rows}x{m_cols} matrix")
+    rng = rng_seed if isinstance(rng_seed, np.random.Generator) else np.random.default_rng(rng_seed)
+    row_idx = np.sort(rng.choice(m_rows, size=n_rows, replace=False))
+    col_idx = np.sort(rng.choice(m_cols, size=n_cols, replace=False))
+    return row_idx, col_idx
+
+
+def index_tensor(idx):
+    return torch.as_tensor(np.ascontiguousarray(idx, dtype=np.int64)).cuda()
+
+
+def gather(mt, rows, cols, out_dtype=None, transpose=False):
+    """mt[np.ix_(rows, cols)] (or its transpose) on the device; rows/cols are host index
+    arrays or None (= all)."""
+    nr = mt.shape[0] if rows is None else len(rows)
+    nc = mt.shape[1] if cols is None else len(cols)
+    odt = out_dtype or mt.dtype
+    out = torch.empty((nc, nr) if transpose else (nr, nc), dtype=odt, device="cuda")
+    rt = None if rows is None else index_tensor(rows)
+    ct = None if cols is None else index_tensor(cols)
+    code_out = _lib.F32 if odt == torch.float32 else _lib.F64
+    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(rt), nr, dv.ptr(ct), nc, code_out,
+              dv.ptr(out), out.stride(0), 1 if transpose else 0, dv.stream())
+    return out
+
+
+def svd_device(t):
+    m, n = t.shape
+    p = min(m, n)
+    u, s, v = dv.empty((m, p)), dv.empty((p,)), dv.empty((n, p))
+    _lib.call("l1f_svd_f64", dv.ptr(t), m, n, t.stride(0), dv.ptr(u), dv.ptr(s), dv.ptr(v), dv.stream(),
+              what=f"SVD failed on {tuple(t.shape)} matrix")
+    return u, s, v
+
+
+def recover_seed_device(block, adm=None, rank_tol=1e-6):
+    """recover_seed (l1filter.py:90-113) on a float64 CUDA block; returns the pieces."""
+    adm = adm or AdmConfig()
+    lam = default_lambda(*block.shape)  # forced 1/sqrt(max dims), l1filter.py:96-98
+    cfg = AdmConfig(lam=lam, tol=adm.tol, beta0=adm.beta0, rho=adm.rho, beta_max=adm.beta_max,
+                    max_iter=adm.max_iter)
+    l, _, info = solve_pcp_device(block, cfg)
+    u, s, v = svd_device(l)
+    sh = s.cpu().numpy()
+    cutoff = rank_tol * (sh[0] if sh.size else 0.0)
+    k = int((sh > cutoff).sum())
+    if k == 0:
+        raise SeedRankZeroError("seed recovery produced a zero low-rank part")
+    u, s, v = u[:, :k].contiguous(), s[:k].contiguous(), v[:, :k].contiguous()
+    seed_l = dv.gemm_nt((u * s.reshape(1, -1)).contiguous(), v)
+    return u, s, v, seed_l, info["iterations"]
+
+
+def seed_stage(mt, cfg):
+    """Seed loop of estimate_rank_and_solve (l1filter.py:185-237).
+
+    Returns ("seed", DeviceSeed, attempts, t1) | ("fallback", proposed, attempts, t1) |
+    ("degenerate", None, attempts, t1).
+    """
+    m_rows, m_cols = mt.shape
+    ss = np.random.SeedSequence(cfg.rng_seed)
+
+    def next_stream():
+        return ss.spawn(1)[0]
+
+    r = max(1, cfg.rank_hint or 1)
+    attempts = 0
+    t1 = 0.0
+    while True:
+        attempts += 1
+        n_rows, n_cols = int(round(cfg.s_r * r)), int(round(cfg.s_c * r))
+        if max(n_rows / m_rows, n_cols / m_cols) > cfg.max_seed_fraction:
+            return "fallback", (n_rows, n_cols), attempts, t1
+        n_rows, n_cols = min(n_rows, m_rows), min(n_cols, m_cols)
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        row_idx, col_idx = sample_indices(m_rows, m_cols, n_rows, n_cols, next_stream())
+        block = gather(mt, row_idx, col_idx, out_dtype=torch.float64)
+        try:
+            u, s, v, seed_l, pcp_it = recover_seed_device(block, cfg.adm, cfg.rank_tol)
+        except SeedRankZeroError:
+            torch.cuda.synchronize()
+            t1 += time.perf_counter() - t0
+            return "degenerate", None, attempts, t1
+        r_prime = int(s.shape[0])
+
+        if cfg.cross_validate:
+            ri2, ci2 = sample_indices(m_rows, m_cols, n_rows, n_cols, next_stream())
+            block2 = gather(mt, ri2, ci2, out_dtype=torch.float64)
+            try:
+                r2 = int(recover_seed_device(block2, cfg.adm, cfg.rank_tol)[1].shape[0])
+            except SeedRankZeroError:
+                r2 = 0
+            if r2 != r_prime:
+                torch.cuda.synchronize()
+                t1 += time.perf_counter() - t0
+                r = max(r_prime, r2, r + 1)
+                continue
+        torch.cuda.synchronize()
+        t1 += time.perf_counter() - t0
+        seed = DeviceSeed(row_idx=row_idx, col_idx=col_idx, u=u, sigma=s, v=v, seed_l=seed_l, block=block,
+                          r_prime=r_prime, pcp_iterations=pcp_it)
+        if n_rows / r_prime >= cfg.s_r and n_cols / r_prime >= cfg.s_c:
+            return "seed", seed, attempts, t1
+        r = max(r_prime, r + 1)  # undersized seed, l1filter.py:237
+
+
+class FilterPlan:
+    """Everything the timed solve needs that does not depend on M's values: index sets on
+    the device, seed factors cast to the working dtype, workspaces and output buffers."""
+
+    def __init__(self, m_rows, m_cols, seed, dtype, adm, want_e=False, row_range=None, col_units=None):
+        self.m_rows, self.m_cols = m_rows, m_cols
+        self.seed = seed
+        self.dtype = dtype
+        self.adm = adm
+        self.want_e = want_e
+        self.k = seed.r_prime
+        r0, r1 = row_range if row_range is not None else (0, m_rows)
+        self.row_range = (r0, r1)
+        comp_rows = np.setdiff1d(np.arange(m_rows), seed.row_idx)
+        comp_cols = np.setdiff1d(np.arange(m_cols), seed.col_idx)
+        self.comp_rows_all, self.comp_cols_all = comp_rows, comp_cols
+        # row units of this shard, column units of this shard (all by default)
+        self.comp_rows = comp_rows[(comp_rows >= r0) & (comp_rows < r1)]
+        self.comp_cols = comp_cols if col_units is None else comp_cols[col_units[0]:col_units[1]]
+        self.d_row_idx = index_tensor(seed.row_idx)
+        self.d_col_idx = index_tensor(seed.col_idx)
+        self.d_comp_cols = index_tensor(self.comp_cols)
+        self.d_comp_rows_local = index_tensor(self.comp_rows - r0)
+        self.u = seed.u.to(dtype).contiguous()
+        self.v = seed.v.to(dtype).contiguous()
+        code = _lib.F32 if dtype == torch.float32 else _lib.F64
+        s_r, s_c = len(seed.row_idx), len(seed.col_idx)
+        nbytes = max(_lib.load().l1f_filter_workspace_bytes(code, s_r, self.k, len(self.comp_cols)),
+                     _lib.load().l1f_filter_workspace_bytes(code, s_c, self.k, len(self.comp_rows)))
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+
+
+def filter_stage(plan, mt, seed_rows=None):
+    """Column and row filtering (l1filter.py:239-248) for the units of ``plan``.
+
+    mt: the (local rows of the) matrix; seed_rows: optional (s_r, n) tensor holding
+    M[row_idx, :] when mt does not contain all seed rows (row-sharded runs).
+    Returns dict(zc, zr, ec, er, iters_c, iters_r, status_c, status_r).
+    """
+    from .l1reg import filter_units
+    r0 = plan.row_range[0]
+    if seed_rows is None:
+        # column panel M[row_idx, comp_cols], unit-major (one column unit per row)
+        xc = torch.empty((len(plan.comp_cols), len(plan.seed.row_idx)), dtype=mt.dtype, device="cuda")
+        _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx),
+                  len(plan.seed.row_idx), dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt),
+                  dv.ptr(xc), xc.stride(0), 1, dv.stream())
+    else:
+        xc = torch.empty((len(plan.comp_cols), seed_rows.shape[0]), dtype=mt.dtype, device="cuda")
+        _lib.call("l1f_gather", dv.dtype_code(seed_rows), dv.ptr(seed_rows), seed_rows.stride(0), None,
+                  seed_rows.shape[0], dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt),
+                  dv.ptr(xc), xc.stride(0), 1, dv.stream())
+    # row panel M[comp_rows, col_idx] (already unit-major)
+    xr = torch.empty((len(plan.comp_rows), len(plan.seed.col_idx)), dtype=mt.dtype, device="cuda")
+    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local),
+              len(plan.comp_rows), dv.ptr(plan.d_col_idx), len(plan.seed.col_idx), dv.dtype_code(mt),
+              dv.ptr(xr), xr.stride(0), 0, dv.stream())
+    ws = plan.workspace
+    zc, ec, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=plan.want_e, workspace=ws)
+    zr, er, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=plan.want_e, workspace=ws)
+    del r0
+    return dict(zc=zc, zr=zr, ec=ec, er=er, iters_c=itc, iters_r=itr, res_c=rc, res_r=rr, status_c=stc,
+                status_r=st_r)
+
+
+def build_factors(plan, zc_all, zr_local):
+    """Af rows for this shard's rows and Bf rows for all columns (unified Nystrom form)."""
+    seed = plan.seed
+    r0, r1 = plan.row_range
+    k = plan.k
+    dt = plan.dtype
+    code = _lib.F32 if dt == torch.float32 else _lib.F64
+    # build over the full index space, then take this shard's rows of Af
+    af_full_rows = r1 - r0
+    bf = torch.empty((plan.m_cols, k), dtype=dt, device="cuda")
+    if r0 == 0 and r1 == plan.m_rows:
+        af = torch.empty((plan.m_rows, k), dtype=dt, device="cuda")
+        _lib.call("l1f_build_factors", code, plan.m_rows, plan.m_cols, k, dv.ptr(plan.d_row_idx),
+                  len(seed.row_idx), dv.ptr(plan.d_col_idx), len(seed.col_idx), dv.ptr(seed.u), dv.ptr(seed.sigma),
+                  dv.ptr(seed.v), dv.ptr(zc_all), zc_all.stride(0), dv.ptr(zr_local), zr_local.stride(0),
+                  dv.ptr(af), dv.ptr(bf), dv.stream())
+        return af, bf
+    # sharded rows: local seed rows / comp rows relative to r0
+    loc = (seed.row_idx >= r0) & (seed.row_idx < r1)
+    local_seed_rows = seed.row_idx[loc] - r0
+    u_local = seed.u[torch.as_tensor(np.flatnonzero(loc), device="cuda")].contiguous()
+    af = torch.empty((af_full_rows, k), dtype=dt, device="cuda")
+    _lib.call("l1f_build_factors", code, af_full_rows, plan.m_cols, k, dv.ptr(index_tensor(local_seed_rows)),
+              len(local_seed_rows), dv.ptr(plan.d_col_idx), len(seed.col_idx), dv.ptr(u_local), dv.ptr(seed.sigma),
+              dv.ptr(seed.v), dv.ptr(zc_all), zc_all.stride(0), dv.ptr(zr_local), zr_local.stride(0),
+              dv.ptr(af), dv.ptr(bf), dv.stream())
+    return af, bf
+
+
+def reconstruct(mt, af, bf, l_out=None, s_out=None):
+    """L = Af Bf^T, S = M - L; returns (L, S, residual_sq(2,) device)."""
+    m, n = mt.shape
+    k = af.shape[1]
+    l_out = l_out if l_out is not None else torch.empty((m, n), dtype=mt.dtype, device="cuda")
+    s_out = s_out if s_out is not None else torch.empty((m, n), dtype=mt.dtype, device="cuda")
+    rs = torch.zeros(2, dtype=torch.float64, device="cuda")
+    _lib.call("l1f_reconstruct", dv.dtype_code(mt), m, n, k, dv.ptr(af), af.stride(0), dv.ptr(bf), bf.stride(0),
+              dv.ptr(mt), mt.stride(0), dv.ptr(l_out), l_out.stride(0), dv.ptr(s_out), s_out.stride(0), dv.ptr(rs),
+              dv.stream())
+    return l_out, s_out, rs
+
+
+def solve_from_seed(mt, plan, l_out=None, s_out=None):
+    """The timed hot path on one GPU: panels -> filters -> factors -> L, S."""
+    f = filter_stage(plan, mt)
+    af, bf = build_factors(plan, f["zc"], f["zr"])
+    l, s, rs = reconstruct(mt, af, bf, l_out, s_out)
+    f.update(l=l, s=s, resid_sq=rs, af=af, bf=bf)
+    return f
+
+
+# ------------------------------------------------------------------ synthetic inputs
+def generate_matrix(m, n, r, rho_s, magnitude, seed=0, kind=_lib.GEN_GAUSSIAN, row0=0, rows=None,
+                    want_l0=False, out=None):
+    """Philox-generated rows [row0, row0+rows) of M = L0 + S0 (fp32 CUDA tensors)."""
+    rows = m - row0 if rows is None else rows
+    x = torch.empty((m, max(r, 1)), dtype=torch.float32, device="cuda")
+    y = torch.empty((n, max(r, 1)), dtype=torch.float32, device="cuda")
+    _lib.call("l1f_generate_factors_f32", int(seed), int(kind), m, n, int(r), dv.ptr(x), dv.ptr(y), dv.stream())
+    mm = out if out is not None else torch.empty((rows, n), dtype=torch.float32, device="cuda")
+    l0 = torch.empty((rows, n), dtype=torch.float32, device="cuda") if want_l0 else None
+    _lib.call("l1f_generate_f32", int(seed), int(kind), m, n, int(r), float(rho_s), float(magnitude), dv.ptr(x),
+              dv.ptr(y), int(row0), int(rows), dv.ptr(mm), mm.stride(0), dv.ptr(l0),
+              l0.stride(0) if l0 is not None else n, dv.stream())
+    return mm, l0, x[:, :r], y[:, :r]
+
+
+def rel_err_device(a, b):
+    """||a - b||_F / ||b||_F on the device (synth.py:92-97)."""
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    _lib.call("l1f_diff_norms", dv.dtype_code(a), dv.ptr(a), a.stride(0), dv.ptr(b), b.stride(0), a.shape[0],
+              a.shape[1], dv.ptr(out), dv.stream())
+    d2, b2 = out.cpu().tolist()
+    return float(np.sqrt(d2) / np.sqrt(b2)) if b2 else float(np.sqrt(d2))
+
+
+def fma_peak_tflops(iters=4096, reps=3):
+    """Measured FP32 FMA throughput of this GPU (the filter kernel's roofline denominator)."""
+    sink = torch.zeros(_sm_count() * 8, dtype=torch.float32, device="cuda")
+    flops = ctypes.c_double(0.0)
+    best = 0.0
+    for _ in range(reps + 1):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.call("l1f_fma_peak_probe", int(iters), dv.ptr(sink), ctypes.addressof(flops), dv.stream())
+        b.record()
+        b.synchronize()
+        best = max(best, flops.value / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def _sm_count():
+    v = ctypes.c_int(0)
+    _lib.call("l1f_sm_count", ctypes.addressof(v))
+    return int(v.value)

@@ -1,0 +1,214 @@
+"""GPU: generator bit-exactness, seed solve, Nystrom/assembly and the full solve against the
+reference's golden outputs and the oracle (reference tests: test_pcp_adm.py,
+test_l1filter.py, test_matcore.py)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1108_5359_b200 as l1pcp
+from conftest import load_golden
+from oracle import philox_gen, pipeline as opipe, ref_synth
+from paper_1108_5359_b200 import _lib, engine
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------- generator
+@pytest.mark.parametrize("kind,m,n,r,rho,mag", [(0, 150, 260, 7, 0.1, 500.0), (0, 33, 45, 0, 0.05, 100.0),
+                                                  (0, 130, 131, 50, 0.05, 500.0), (1, 640, 24, 3, 0.0, 255.0)])
+def test_generator_bit_exact_against_oracle(kind, m, n, r, rho, mag):
+    mm, l0, x, y = engine.generate_matrix(m, n, r, rho, mag, seed=11, kind=kind, want_l0=True)
+    xo, yo = philox_gen.factors(11, kind, m, n, r)
+    np.testing.assert_array_equal(x.cpu().numpy(), xo)
+    np.testing.assert_array_equal(y.cpu().numpy(), yo)
+    mo, l0o = philox_gen.block(11, kind, m, n, r, rho, mag, np.arange(m), np.arange(n), x=xo, y=yo, want_l0=True)
+    np.testing.assert_array_equal(l0.cpu().numpy(), l0o)
+    np.testing.assert_array_equal(mm.cpu().numpy(), mo)
+
+
+def test_generator_row_shards_compose():
+    m, n, r = 300, 200, 5
+    full, _, _, _ = engine.generate_matrix(m, n, r, 0.1, 500.0, seed=3)
+    a, _, _, _ = engine.generate_matrix(m, n, r, 0.1, 500.0, seed=3, row0=0, rows=131)
+    b, _, _, _ = engine.generate_matrix(m, n, r, 0.1, 500.0, seed=3, row0=131, rows=169)
+    assert torch.equal(torch.cat([a, b]), full)
+
+
+# ---------------------------------------------------------------- dense primitives
+def test_matcore_basics():
+    assert l1pcp.frobenius_norm([[3, 0], [0, 4]]) == pytest.approx(5.0)
+    assert l1pcp.l1_norm([[1, -2], [0, 3]]) == 6.0
+    assert l1pcp.l0_count([[1, -2], [0, 3]], 0.0) == 3
+    assert l1pcp.linf_norm([[1, -2], [0, 3]]) == 3.0
+    assert l1pcp.l0_count(np.array([[100.0, 1e-5], [0.0, 0.0]])) == 1
+    assert l1pcp.soft_threshold(np.array([[3.0]]), 1.0)[0, 0] == 2.0
+    assert l1pcp.soft_threshold(np.array([[-0.5]]), 1.0)[0, 0] == 0.0
+    m = np.random.default_rng(0).standard_normal((6, 5))
+    np.testing.assert_array_equal(l1pcp.soft_threshold(m, 0.0), m)
+
+
+def test_svd_svt_pinv():
+    f = l1pcp.svd(np.diag([3.0, 1.0]), rank_tol=0.0)
+    np.testing.assert_allclose(f.sigma, [3.0, 1.0])
+    a, b = np.array([1.0, 2.0, 2.0]), np.array([0.0, 3.0, 4.0])
+    f = l1pcp.svd(np.outer(a, b))
+    assert f.rank == 1 and f.sigma[0] == pytest.approx(15.0)
+    rng = np.random.default_rng(2)
+    for shape in [(20, 10), (50, 50), (200, 120), (120, 200)]:
+        m = rng.standard_normal(shape)
+        f = l1pcp.svd(m, rank_tol=0.0)
+        assert np.linalg.norm(f.reconstruct() - m) <= 1e-8 * np.linalg.norm(m)
+        np.testing.assert_allclose(f.u.T @ f.u, np.eye(f.rank), atol=1e-10)
+    np.testing.assert_allclose(l1pcp.svt(np.diag([3.0, 1.0]), 2.0), np.diag([1.0, 0.0]), atol=1e-12)
+    w = rng.standard_normal((12, 9))
+    sig = np.linalg.svd(w, compute_uv=False)
+    assert l1pcp.nuclear_norm(l1pcp.svt(w, 0.7)) == pytest.approx(np.maximum(sig - 0.7, 0).sum(), abs=1e-9)
+    g1, g2 = rng.standard_normal((20, 3)), rng.standard_normal((15, 3))
+    l = g1 @ g2.T
+    rhs = l @ rng.standard_normal((15, 4))
+    y = l1pcp.pseudo_inverse_apply(l1pcp.svd(l), rhs)
+    assert np.linalg.norm(l @ y - rhs) <= 1e-8 * np.linalg.norm(rhs)
+
+
+# ---------------------------------------------------------------- seed
+def test_spectral_norm_and_zero_pcp():
+    assert l1pcp.pcp_adm.spectral_norm_estimate(np.diag([5.0, 2.0, 1.0])) == pytest.approx(5.0, rel=1e-6)
+    assert l1pcp.pcp_adm.spectral_norm_estimate(np.zeros((3, 3))) == 0.0
+    sol = l1pcp.solve_pcp(np.zeros((10, 10)))
+    assert sol.converged and sol.iterations == 1 and sol.rank_of_l == 0 and not sol.l.any()
+
+
+def test_pcp_matches_reference_golden():
+    d, meta = load_golden("pcp_rect")
+    sol = l1pcp.solve_pcp(d["m"])
+    assert sol.converged == meta["converged"]
+    assert abs(sol.iterations - meta["iterations"]) <= 1
+    assert sol.rank_of_l == meta["rank"]
+    assert np.linalg.norm(sol.l - d["l"]) <= 1e-6 * np.linalg.norm(d["l"])
+    assert np.linalg.norm(sol.s - d["s"]) <= 1e-6 * np.linalg.norm(d["s"])
+    assert l1pcp.pcp_adm.spectral_norm_estimate(d["m"]) == pytest.approx(meta["spectral"], rel=1e-10)
+
+
+@pytest.mark.parametrize("name", ["seed_clean_rank2", "seed_corrupt_rank5"])
+def test_recover_seed_matches_reference_golden(name):
+    d, meta = load_golden(name)
+    seed = l1pcp.recover_seed(d["block"], l1pcp.AdmConfig(tol=meta["tol"]))
+    assert seed.r_prime == meta["r_prime"]
+    assert abs(seed.pcp_iterations - meta["pcp_iterations"]) <= 1
+    np.testing.assert_allclose(seed.seed_svd.sigma, d["sigma"], rtol=1e-6)
+    assert np.linalg.norm(seed.seed_l - d["seed_l"]) <= 1e-6 * np.linalg.norm(d["seed_l"])
+
+
+def test_recover_seed_zero_block_raises():
+    with pytest.raises(l1pcp.SeedRankZeroError):
+        l1pcp.recover_seed(np.zeros((20, 20)))
+
+
+def test_max_iter_exhaustion_is_flagged():
+    m, _, _ = ref_synth.generate(100, 100, 0.03, 0.05, rng_seed=0)
+    sol = l1pcp.solve_pcp(m, l1pcp.AdmConfig(tol=1e-12, max_iter=3))
+    assert not sol.converged and sol.iterations == 3 and sol.final_residual > 1e-12
+
+
+# ---------------------------------------------------------------- Nystrom / assembly
+def test_nystrom_and_assembly_match_reference_golden():
+    d, meta = load_golden("nystrom_exact")
+    f = l1pcp.SkinnySvd(u=d["u"], sigma=d["sigma"], v=d["v"])
+    seed = l1pcp.SeedRecovery(row_idx=d["row_idx"], col_idx=d["col_idx"], seed_svd=f, seed_l=f.reconstruct(),
+                              seed_s=None, r_prime=meta["r_prime"])
+    fr = l1pcp.FilterResult(q_tilde=d["q"], p_tilde=d["p"], s_col=None, s_row=None)
+    comp = l1pcp.nystrom_complete(seed, fr)
+    np.testing.assert_allclose(comp, d["completion"], rtol=0, atol=1e-12 * np.abs(comp).max())
+    l_hat = l1pcp.assemble(seed, fr, comp, 80, 70)
+    np.testing.assert_allclose(l_hat, d["l_hat"], rtol=0, atol=1e-12 * np.abs(l_hat).max())
+    # exact re-extraction of the placed blocks (test_l1filter.py:164-177)
+    np.testing.assert_array_equal(l_hat[np.ix_(d["row_idx"], d["col_idx"])], seed.seed_l)
+    comp_r = np.setdiff1d(np.arange(80), d["row_idx"])
+    comp_c = np.setdiff1d(np.arange(70), d["col_idx"])
+    np.testing.assert_array_equal(l_hat[np.ix_(comp_r, comp_c)], comp)
+    with pytest.raises(RuntimeError):
+        l1pcp.assemble(seed, fr, np.zeros((5, 5)), 80, 70)
+
+
+def test_filter_columns_rows_exact_subspace():
+    rng = np.random.default_rng(3)
+    u, _ = np.linalg.qr(rng.standard_normal((40, 3)))
+    q0 = rng.standard_normal((3, 15))
+    q, s_col, _ = l1pcp.filter_columns(u @ q0, u, l1pcp.AdmConfig(tol=1e-10))
+    assert np.abs(s_col).max() <= 1e-8 and np.abs(q - q0).max() <= 1e-6
+    v, _ = np.linalg.qr(rng.standard_normal((30, 3)))
+    p0 = rng.standard_normal((3, 12))
+    p, s_row, _ = l1pcp.filter_rows(p0.T @ v.T, v, l1pcp.AdmConfig(tol=1e-10))
+    assert s_row.shape == (12, 30) and np.abs(s_row).max() <= 1e-8 and np.abs(p - p0).max() <= 1e-6
+    q, s_col, it = l1pcp.filter_columns(np.zeros((40, 0)), u)
+    assert q.shape == (3, 0) and s_col.shape == (40, 0) and it == 0
+
+
+# ---------------------------------------------------------------- full solve
+@pytest.mark.parametrize("name", ["pipeline_hint", "pipeline_rect_norank", "pipeline_tol7"])
+def test_full_solve_matches_reference_golden(name):
+    d, meta = load_golden(name)
+    m, l0, _ = ref_synth.generate(**meta["spec"])
+    assert hashlib.sha256(m.tobytes()).hexdigest() == meta["m_sha256"]
+    cfg = l1pcp.FilterConfig(rank_hint=meta["rank_hint"], rng_seed=meta["rng_seed"],
+                             adm=l1pcp.AdmConfig(tol=meta["tol"]))
+    sol = l1pcp.estimate_rank_and_solve(m, cfg)
+    assert sol.method == meta["method"] == "l1-filter"
+    assert sol.rank_of_l == meta["rank"]
+    assert sol.stats["seed_rows"] == meta["stats"]["seed_rows"]
+    assert sol.stats["attempts"] == meta["stats"]["attempts"]
+    assert np.linalg.norm(sol.l - d["l"]) <= 1e-6 * np.linalg.norm(d["l"])
+    s_ref = m - d["l"]
+    assert np.linalg.norm(sol.s - s_ref) <= 1e-6 * np.linalg.norm(s_ref)
+    np.testing.assert_allclose(sol.l + sol.s, m, atol=1e-10)
+    assert sol.final_residual == 0.0
+    assert l1pcp.rel_err(sol.l, l0) <= max(1e-5, 10 * meta["rel_err"])
+
+
+def test_full_solve_float32_tensor_path_matches_oracle():
+    d, meta = load_golden("pipeline_tol7")
+    m, _, _ = ref_synth.generate(**meta["spec"])
+    mt = torch.from_numpy(m.astype(np.float32)).cuda()
+    cfg = l1pcp.FilterConfig(rank_hint=meta["rank_hint"], rng_seed=meta["rng_seed"],
+                             adm=l1pcp.AdmConfig(tol=1e-7))
+    sol = l1pcp.estimate_rank_and_solve(mt, cfg)
+    assert sol.l.dtype == torch.float32 and sol.l.is_cuda
+    ref = opipe.solve(mt.double().cpu().numpy(), meta["rank_hint"], meta["rng_seed"], tol=1e-7)
+    l = sol.l.double().cpu().numpy()
+    s = sol.s.double().cpu().numpy()
+    assert np.linalg.norm(l - ref["l"]) <= 1e-4 * np.linalg.norm(ref["l"])
+    assert np.linalg.norm(s - ref["s"]) <= 1e-4 * np.linalg.norm(ref["s"])
+
+
+def test_degenerate_zero_matrix():
+    sol = l1pcp.estimate_rank_and_solve(np.zeros((50, 50)), l1pcp.FilterConfig(rng_seed=0))
+    assert sol.method == "degenerate-zero-seed" and sol.rank_of_l == 0 and not sol.l.any()
+
+
+def test_fallback_to_full_pcp_for_high_rank():
+    m, _, _ = ref_synth.generate(100, 100, 0.4, 0.01, rng_seed=0)
+    sol = l1pcp.estimate_rank_and_solve(m, l1pcp.FilterConfig(rng_seed=0))
+    assert sol.method == "full-pcp-fallback"
+    assert np.linalg.norm(m - sol.l - sol.s) / np.linalg.norm(m) <= 1e-7
+
+
+def test_end_to_end_with_device_generated_instance():
+    gt = l1pcp.generate(l1pcp.SynthSpec(m=300, n=300, rho_r=0.01, rho_s=0.01, rng_seed=0))
+    sol = l1pcp.estimate_rank_and_solve(gt.m_obs, l1pcp.FilterConfig(rank_hint=3, rng_seed=0))
+    assert sol.method == "l1-filter" and sol.rank_of_l == 3
+    assert l1pcp.rel_err(sol.l, gt.l0) <= 1e-5
+    np.testing.assert_allclose(sol.l + sol.s, gt.m_obs, atol=1e-10)
+
+
+def test_rank_estimation_and_cross_validation():
+    m, l0, _ = ref_synth.generate(400, 400, 0.005, 0.01, rng_seed=1)
+    sol = l1pcp.estimate_rank_and_solve(m, l1pcp.FilterConfig(rng_seed=3))
+    assert sol.method == "l1-filter" and sol.rank_of_l == 2 and sol.stats["seed_rows"] >= 20
+    assert l1pcp.rel_err(sol.l, l0) <= 1e-5
+    m, l0, _ = ref_synth.generate(300, 300, 0.01, 0.01, rng_seed=2)
+    sol = l1pcp.estimate_rank_and_solve(m, l1pcp.FilterConfig(rng_seed=0, cross_validate=True))
+    assert sol.method == "l1-filter" and sol.rank_of_l == 3
+    assert l1pcp.rel_err(sol.l, l0) <= 1e-5
