@@ -1,0 +1,441 @@
+"""Benchmark of the l1-filtering PCP hot path on B200 (metric of BASELINE.json:
+M entries/s = m*n / solve time, plus roofline fractions).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One "step" is one pass of the hot path over the synthetic input of config C (default 3):
+panel gathers -> column + row ADM filtering -> rank-k factor build -> reconstruction
+L = Af Bf^T, S = M - L (+ residual).  The seed PCP (t1) is solved once before the timed
+steps and reported separately (solve time runs from "seed factors resident" to
+"L and S written").  M (Philox, fp32) is larger than L2 for configs 2-5, so no flush is
+needed between steps.
+
+--impl reference times the reference algorithm's CPU implementation (the numpy oracle,
+a restatement of /root/reference/pkg/src/l1pcp) on the host cores, on a bounded sample of
+the same workload, extrapolated to the full matrix.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "M entries/s (m*n / solve time)"
+UNIT = "M entries/s"
+TOL = 1e-7  # BASELINE.json: ALM tolerance 1e-7
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-units", type=int, default=0, help="units per filter in the CPU sample")
+    return p.parse_args()
+
+
+def cfg_of(c):
+    from paper_1108_5359_b200.synth import BENCHMARK_CONFIGS
+    return dict(BENCHMARK_CONFIGS[c])
+
+
+def workload_name(cfg):
+    return (f"{cfg['name']}: {cfg['m']}x{cfg['n']} r={cfg['r']} "
+            f"{'video boxes' if cfg['kind'] else f'rho_s={cfg['rho_s']}'} seed {10 * cfg['r']}^2 tol {TOL}")
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------- CPU (oracle) sample
+def cpu_sample(cfgd, seed_np, m_rows, m_cols, n_units, threads):
+    """Time the reference algorithm (numpy oracle) on a bounded sample of the workload:
+    the ADM filter on n_units column units and n_units row units plus the reconstruction
+    of a block of rows; extrapolate to the whole matrix.  Returns dict."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import adm_filter, philox_gen
+
+    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
+    ri, ci = seed_np["row_idx"], seed_np["col_idx"]
+    u, sig, v = seed_np["u"], seed_np["sigma"], seed_np["v"]
+    comp_r = np.setdiff1d(np.arange(m), ri)
+    comp_c = np.setdiff1d(np.arange(n), ci)
+    rng = np.random.default_rng(1)
+    sc = np.sort(rng.choice(comp_c, min(n_units, comp_c.size), replace=False))
+    sr = np.sort(rng.choice(comp_r, min(n_units, comp_r.size), replace=False))
+    x, y = philox_gen.factors(0, cfgd["kind"], m, n, r)
+
+    def blk(rows, cols):
+        return philox_gen.block(0, cfgd["kind"], m, n, r, cfgd["rho_s"], cfgd["magnitude"], rows, cols, x=x,
+                                y=y).astype(np.float64)
+
+    xc = blk(ri, sc)
+    xr = blk(sr, ci).T.copy()
+    recon_rows = max(1, min(m, int(4e6 // n)))
+    mrec = blk(np.arange(recon_rows), np.arange(n))
+
+    def chunked(xp, a):
+        # the reference's fixed 64-column chunks on a thread pool (l1reg.py:183-196)
+        bounds = list(range(0, xp.shape[1], 64)) + [xp.shape[1]]
+        chunks = [(lo, hi) for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]
+
+        def run(c):
+            return adm_filter.solve_units(xp[:, c[0]:c[1]], a, TOL)
+
+        if threads <= 1:
+            return [run(c) for c in chunks]
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            return list(pool.map(run, chunks))
+
+    t0 = time.perf_counter()
+    outc = chunked(xc, u)
+    outr = chunked(xr, v)
+    t_filter = time.perf_counter() - t0
+    q = np.concatenate([o[0] for o in outc], axis=1)
+    p = np.concatenate([o[0] for o in outr], axis=1)
+    # reconstruction of recon_rows x n: a_i . b_j then S = M - L (l1filter.py:250-254)
+    a_rows = np.tile(p[:, :1].T / sig, (recon_rows, 1))
+    b_cols = np.tile(q[:, :1].T, (n, 1))
+    t0 = time.perf_counter()
+    l = a_rows @ b_cols.T
+    s = mrec - l
+    t_recon = time.perf_counter() - t0
+    del s
+    units_total = comp_c.size + comp_r.size
+    t_est = t_filter / (sc.size + sr.size) * units_total + t_recon / recon_rows * m
+    return {"t_filter_sample": t_filter, "t_recon_sample": t_recon, "units_sampled": int(sc.size + sr.size),
+            "units_total": int(units_total), "recon_rows": recon_rows, "t_est": t_est,
+            "value": m * n / t_est / 1e6}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import philox_gen, seed_pcp
+
+    cfgd = cfg_of(args.config)
+    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
+    threads = len(os.sched_getaffinity(0))
+    # seed (untimed, as in the GPU arm): regenerate the seed block on the host
+    from oracle.pipeline import sample_indices
+    ss = np.random.SeedSequence(0)
+    ri, ci = sample_indices(m, n, 10 * r, 10 * r, ss.spawn(1)[0])
+    x, y = philox_gen.factors(0, cfgd["kind"], m, n, r)
+    block = philox_gen.block(0, cfgd["kind"], m, n, r, cfgd["rho_s"], cfgd["magnitude"], ri, ci, x=x, y=y)
+    rec = seed_pcp.recover(block.astype(np.float64), tol=TOL)
+    seed_np = {"row_idx": ri, "col_idx": ci, "u": rec[0], "sigma": rec[1], "v": rec[2]}
+    units = args.cpu_sample_units or default_cpu_units(cfgd)
+    times = []
+    for i in range(args.warmup + args.steps):
+        out = cpu_sample(cfgd, seed_np, m, n, units, threads)
+        if i >= args.warmup:
+            times.append(out["t_est"])
+    t = float(np.mean(times))
+    value = m * n / t / 1e6
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox, BASELINE.json config)",
+            "config": {"workload": workload_name(cfgd), "parallelism": f"cpu threads={threads}"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{units} column + {units} row ADM units and a {out['recon_rows']}-row "
+                                       f"reconstruction block per step, extrapolated to {out['units_total']} "
+                                       f"units / {m}x{n} entries; seed solved once, untimed"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def default_cpu_units(cfgd):
+    s, k = 10 * cfgd["r"], cfgd["r"]
+    # ~1 s of numpy per 64-unit chunk at s=1000,k=100; keep the sample near 10-20 s
+    work = s * k
+    return int(max(64, min(2048, 64 * round(2.0e6 * 64 / max(work, 1) / 64))))
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1108_5359_b200 as l1pcp
+    from paper_1108_5359_b200 import engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1108_5359_b200 import distributed as pdist
+        return pdist.run_bench(args, rank, world)
+
+    cfgd = cfg_of(args.config)
+    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
+    peaks = measured_peaks()
+    fma_tflops = engine.fma_peak_tflops()
+
+    # input: Philox on the device
+    t0 = time.perf_counter()
+    mt, _, _, _ = engine.generate_matrix(m, n, r, cfgd["rho_s"], cfgd["magnitude"], seed=0, kind=cfgd["kind"])
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+
+    fcfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=TOL))
+    kind, seed, attempts, t1 = engine.seed_stage(mt, fcfg)
+    if kind != "seed":
+        raise RuntimeError(f"seed stage ended in {kind}")
+    plan = engine.FilterPlan(m, n, seed, mt.dtype, fcfg.adm, want_e=False)
+    l_out = torch.empty_like(mt)
+    s_out = torch.empty_like(mt)
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        from paper_1108_5359_b200 import _device as dv  # noqa: F401
+        f = engine.filter_stage(plan, mt) if evs is None else _staged(plan, mt, evs)
+        af, bf = engine.build_factors(plan, f["zc"], f["zr"])
+        if evs is not None:
+            evs[3].record(stream)
+        _, _, rs = engine.reconstruct(mt, af, bf, l_out, s_out)
+        if evs is not None:
+            evs[4].record(stream)
+        return f, rs
+
+    for _ in range(args.warmup):
+        f, rs = step()
+    torch.cuda.synchronize()
+
+    ev_all = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            f, rs = step(ev_all[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    t_filter = np.mean([e[0].elapsed_time(e[2]) for e in ev_all]) if ev_all else 0.0  # gathers excluded below
+    t_filter_only = np.mean([e[1].elapsed_time(e[2]) for e in ev_all])
+    t_recon = np.mean([e[3].elapsed_time(e[4]) for e in ev_all])
+    value = m * n / (ms * 1e-3) / 1e6
+
+    # algorithmic work of the dominant kernel: sum_u it_u * s * (4k + 12)
+    k = seed.r_prime
+    itc = f["iters_c"].double().sum().item()
+    itr = f["iters_r"].double().sum().item()
+    s_r, s_c = len(seed.row_idx), len(seed.col_idx)
+    flops = itc * s_r * (4 * k + 12) + itr * s_c * (4 * k + 12)
+    achieved = flops / (t_filter_only * 1e-3) / 1e12
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    recon_bytes = 12.0 * m * n
+    recon_gbs = recon_bytes / (t_recon * 1e-3) / 1e9
+    failed = int(((f["status_c"] == 1) | (f["status_c"] == 2)).sum().item()
+                 + ((f["status_r"] == 1) | (f["status_r"] == 2)).sum().item())
+    r2, m2 = rs.cpu().tolist()
+
+    # e2e: host (pinned) M in, L and S out, through the same solve
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(mt, plan, args, l_out, s_out)
+
+    # recovery error vs L0 (reported, not gated): regenerate L0 on the device
+    rel = recovery_error(cfgd, l_out)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        seed_np = {"row_idx": seed.row_idx, "col_idx": seed.col_idx, "u": seed.u.cpu().numpy(),
+                   "sigma": seed.sigma.cpu().numpy(), "v": seed.v.cpu().numpy()}
+        threads = len(os.sched_getaffinity(0))
+        units = args.cpu_sample_units or default_cpu_units(cfgd)
+        out = cpu_sample(cfgd, seed_np, m, n, units, threads)
+        cpu = {"value": out["value"], "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{out['units_sampled']} ADM units (numpy oracle, 64-unit chunks on {threads} threads) + "
+                         f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
+                         f"{m}x{n}"}
+
+    launches_per_step = 2 + 2 * 3 + 1 + 2
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Philox4x64-10 on device; BASELINE.json config statistics)",
+        "config": {"workload": workload_name(cfgd), "m": m, "n": n, "rank": r, "seed_block": [s_r, s_c],
+                   "r_prime": k, "tol": TOL, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (M is %.1f GB)" % (m * n * 4 / 1e9)},
+        "roofline": {"bound": "fp32", "kernel": "adm_filter_kernel (column + row filters)", "achieved": achieved,
+                     "peak": fma_tflops, "unit": "TFLOP/s", "frac": achieved / fma_tflops,
+                     "peak_source": "measured FP32 FMA probe (l1f_fma_peak_probe, this run)",
+                     "peak_nominal": 148 * 128 * 2 * 1.965e9 / 1e12, "traffic": None,
+                     "algorithmic_flops_per_step": flops, "kernel_ms_per_step": t_filter_only},
+        "roofline_reconstruct": {"bound": "hbm", "achieved": recon_gbs, "peak": hbm, "unit": "GB/s",
+                                 "frac": recon_gbs / hbm, "bytes_per_step": recon_bytes, "kernel_ms_per_step": t_recon,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+        "phases_ms": {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
+                      "filters": t_filter_only, "factors": float(np.mean([e[2].elapsed_time(e[3]) for e in ev_all])),
+                      "reconstruct": t_recon, "t1_seed_s": t1, "generate_s": t_gen},
+        "filter": {"units": int(f["iters_c"].numel() + f["iters_r"].numel()),
+                   "mean_iters": (itc + itr) / max(1, f["iters_c"].numel() + f["iters_r"].numel()),
+                   "max_iters": int(max(f["iters_c"].max().item(), f["iters_r"].max().item())),
+                   "failed_units": failed},
+        "recovery_rel_err": rel, "residual": float(np.sqrt(r2 / m2)) if m2 else 0.0,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def _staged(plan, mt, evs):
+    """filter_stage with events: evs[0] start, evs[1] after gathers, evs[2] after filters."""
+    import torch
+    from paper_1108_5359_b200 import _device as dv, _lib
+    from paper_1108_5359_b200.l1reg import filter_units
+    stream = torch.cuda.current_stream()
+    evs[0].record(stream)
+    xc = torch.empty((len(plan.comp_cols), len(plan.seed.row_idx)), dtype=mt.dtype, device="cuda")
+    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx),
+              len(plan.seed.row_idx), dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt), dv.ptr(xc),
+              xc.stride(0), 1, dv.stream())
+    xr = torch.empty((len(plan.comp_rows), len(plan.seed.col_idx)), dtype=mt.dtype, device="cuda")
+    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local),
+              len(plan.comp_rows), dv.ptr(plan.d_col_idx), len(plan.seed.col_idx), dv.dtype_code(mt), dv.ptr(xr),
+              xr.stride(0), 0, dv.stream())
+    evs[1].record(stream)
+    zc, _, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=False, workspace=plan.workspace)
+    zr, _, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=False, workspace=plan.workspace)
+    evs[2].record(stream)
+    return dict(zc=zc, zr=zr, iters_c=itc, iters_r=itr, status_c=stc, status_r=st_r)
+
+
+def run_e2e(mt, plan, args, l_dev, s_dev):
+    """Same solve with host buffers: pinned M in, L and S out, copies inside the timed region."""
+    import torch
+    from paper_1108_5359_b200 import engine
+    m_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
+    m_host.copy_(mt)
+    l_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
+    s_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
+    m_dev = torch.empty_like(mt)
+    stream = torch.cuda.current_stream()
+    steps = max(1, min(args.steps, 3))
+
+    def one():
+        m_dev.copy_(m_host, non_blocking=True)
+        engine.solve_from_seed(m_dev, plan, l_dev, s_dev)
+        l_host.copy_(l_dev, non_blocking=True)
+        s_host.copy_(s_dev, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nbytes = mt.numel() * mt.element_size()
+    return {"value": mt.numel() / (ms * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": 2 * nbytes, "ms_per_step": ms, "steps": steps,
+            "path": "pinned host M -> H2D -> panels/filters/factors/reconstruct -> D2H L, S"}
+
+
+def recovery_error(cfgd, l_out):
+    import torch
+    from paper_1108_5359_b200 import engine
+    m, n = l_out.shape
+    rows = min(m, 4096)
+    _, l0, _, _ = engine.generate_matrix(cfgd["m"], cfgd["n"], cfgd["r"], cfgd["rho_s"], cfgd["magnitude"], seed=0,
+                                         kind=cfgd["kind"], rows=rows, want_l0=True)
+    out = engine.rel_err_device(l_out[:rows].contiguous(), l0)
+    del l0
+    torch.cuda.empty_cache()
+    return {"value": out, "rows_checked": rows}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

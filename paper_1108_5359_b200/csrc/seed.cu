@@ -144,14 +144,10 @@ static int svd_rowmajor(Handles* h, const double* W, int64_t m, int64_t n, int64
   const int R = (int)(wide ? n : m), C = (int)(wide ? m : n);
   Buf a(st), ucm(st), vtcm(st), work(st), info(st);
   L1F_CUDA_TRY(a.alloc(sizeof(double) * (size_t)R * C));
-  const double one = 1.0, zero = 0.0;
-  if (wide) {
-    // column-major R x C with ld R: A(j, i) = W[i][j]  -> W rows are A columns
-    cublasDgeam(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, R, C, &one, W, (int)ldw, &zero, W, (int)ldw, a.d(), R);
-  } else {
-    // column-major m x n = transpose of the (n x m col-major) view of W
-    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, R, C, &one, W, (int)ldw, &zero, W, (int)ldw, a.d(), R);
-  }
+  // column-major copy for gesvd via our gather kernel (row-major W is col-major W^T)
+  int rc = wide ? l1f_gather(L1F_F64, W, ldw, nullptr, m, nullptr, n, L1F_F64, a.d(), n, 0, st)
+                : l1f_gather(L1F_F64, W, ldw, nullptr, m, nullptr, n, L1F_F64, a.d(), m, 1, st);
+  if (rc) return rc;
   L1F_CUDA_TRY(ucm.alloc(sizeof(double) * (size_t)R * p));
   L1F_CUDA_TRY(vtcm.alloc(sizeof(double) * (size_t)p * C));
   int lwork = 0;
@@ -175,13 +171,16 @@ static int svd_rowmajor(Handles* h, const double* W, int64_t m, int64_t n, int64
     return L1F_ERR_SVD;
   }
   if (wide) {
-    // left vectors of W^T are V (n x p col-major) ; VT^T = U (p x m col-major == m x p row-major)
+    // left vectors of W^T are V (n x p col-major == p x n row-major); VT (p x m col-major)
+    // is U as an m x p row-major matrix
     L1F_CUDA_TRY(cudaMemcpyAsync(U, vtcm.p, sizeof(double) * (size_t)p * C, cudaMemcpyDeviceToDevice, st));
-    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, R, &one, ucm.d(), R, &zero, ucm.d(), R, V, (int)p);
+    rc = l1f_gather(L1F_F64, ucm.d(), R, nullptr, p, nullptr, R, L1F_F64, V, p, 1, st);
   } else {
-    cublasDgeam(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, R, &one, ucm.d(), R, &zero, ucm.d(), R, U, (int)p);
+    rc = l1f_gather(L1F_F64, ucm.d(), R, nullptr, p, nullptr, R, L1F_F64, U, p, 1, st);
+    if (rc) return rc;
     L1F_CUDA_TRY(cudaMemcpyAsync(V, vtcm.p, sizeof(double) * (size_t)p * C, cudaMemcpyDeviceToDevice, st));
   }
+  if (rc) return rc;
   L1F_CHECK_LAUNCH();
   return L1F_OK;
 }
