@@ -311,7 +311,9 @@ def run_ours(args):
 
     # e2e: host (pinned) M in, L and S out, through the same solve
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and 3 * mt.numel() * mt.element_size() > 0.5 * _host_ram_bytes():
+        e2e = {"value": None, "unit": UNIT, "skipped": "3 pinned host copies of M exceed half the host RAM"}
+    elif not args.no_e2e:
         e2e = run_e2e(mt, plan, args, l_out, s_out)
 
     # recovery error vs L0 (reported, not gated): regenerate L0 on the device
@@ -415,6 +417,13 @@ def run_e2e(mt, plan, args, l_dev, s_dev):
     return {"value": mt.numel() / (ms * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": nbytes,
             "d2h_bytes_per_step": 2 * nbytes, "ms_per_step": ms, "steps": steps,
             "path": "pinned host M -> H2D -> panels/filters/factors/reconstruct -> D2H L, S"}
+
+
+def _host_ram_bytes():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 0
 
 
 def recovery_error(cfgd, l_out):

@@ -23,6 +23,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace l1f {
 namespace filt {
@@ -57,6 +58,12 @@ template <> struct V4<double> {
 
 template <typename T>
 __device__ __forceinline__ T recip(T b) { return T(1) / b; }
+
+// L1F_FILTER_KERNEL=streaming forces the streaming kernel (A/B comparisons, tests)
+inline bool force_streaming() {
+  const char* v = getenv("L1F_FILTER_KERNEL");
+  return v && v[0] == 's';
+}
 
 struct Params {
   int s, s_pad, k, kp;
@@ -415,6 +422,33 @@ int dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_
 #undef L1F_KJ
 }
 
+}  // namespace filt
+}  // namespace l1f
+
+template <typename T>
+int l1f_resident_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k,
+                          double tol, double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz,
+                          T* E, int64_t lde, int32_t* iters, T* res, uint8_t* status, void* workspace,
+                          size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+
+namespace l1f {
+namespace filt {
+
+// resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
+template <typename T>
+int select(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
+           double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
+           int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
+           bool query, size_t* need) {
+  if (!force_streaming()) {
+    const int rc = l1f_resident_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z,
+                                            ldz, E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
+    if (rc != L1F_ERR_UNSUPPORTED) return rc;
+  }
+  return dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, iters,
+                     res, status, workspace, ws_bytes, st, query, need);
+}
+
 template <typename T>
 int filter_entry(const T* X, int64_t ldx, int32_t s, int64_t n_units, const T* A, int64_t lda, int32_t k, T tol,
                  T rho, T beta0, T beta_max, int32_t max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
@@ -424,7 +458,7 @@ int filter_entry(const T* X, int64_t ldx, int32_t s, int64_t n_units, const T* A
   L1F_REQUIRE(n_units < (int64_t)INT32_MAX, L1F_ERR_UNSUPPORTED, "filter: too many units");
   L1F_REQUIRE(rho > T(1) && tol > T(0), L1F_ERR_ARG, "filter: need rho > 1 and tol > 0");
   if (n_units == 0) return L1F_OK;
-  return dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, iters,
+  return select<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, iters,
                      res, status, workspace, ws_bytes, (cudaStream_t)stream, false, nullptr);
 }
 
@@ -437,10 +471,10 @@ extern "C" size_t l1f_filter_workspace_bytes(int dtype, int32_t s, int32_t k, in
   size_t need = 0;
   if (s < 1 || k < 1 || n_units < 0) return 0;
   if (dtype == L1F_F32)
-    filt::dispatch<float>(nullptr, s, s, n_units, nullptr, k, k, 1e-7, 1.5, 0, 0, 1, nullptr, k, nullptr, s,
+    filt::select<float>(nullptr, s, s, n_units, nullptr, k, k, 1e-7, 1.5, 0, 0, 1, nullptr, k, nullptr, s,
                           nullptr, nullptr, nullptr, nullptr, 0, nullptr, true, &need);
   else
-    filt::dispatch<double>(nullptr, s, s, n_units, nullptr, k, k, 1e-7, 1.5, 0, 0, 1, nullptr, k, nullptr, s,
+    filt::select<double>(nullptr, s, s, n_units, nullptr, k, k, 1e-7, 1.5, 0, 0, 1, nullptr, k, nullptr, s,
                            nullptr, nullptr, nullptr, nullptr, 0, nullptr, true, &need);
   return need;
 }
