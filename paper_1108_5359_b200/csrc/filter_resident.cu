@@ -62,12 +62,17 @@ struct Params {
   double tol, rho, beta0, beta_max;
 };
 
+constexpr int RING = 4;  // prefetched upcoming units per cluster
+
 template <typename T>
 struct Slots {
-  int unit[TS], it[TS], stalled[TS], state[TS], finish[TS];
-  T beta_cur[TS], beta_next[TS], inv_next[TS], beta_max[TS], thresh[TS], prev_res[TS], res[TS], rloc[TS];
+  int unit[TS], it[TS], stalled[TS], state[TS], finish[TS], src[TS];
+  T beta_cur[TS], beta_next[TS], inv_next[TS], beta_max[TS], thresh[TS], prev_res[TS], res[TS];
+  T ring_sc[RING];
+  long long ring_u[RING];
+  long long head, tail, pf_from, pf_to;  // candidate cursor of this cluster (identical in all its CTAs)
+  alignas(8) unsigned long long bar_p, bar_r;  // mbarriers of the DSMEM z reduction
   uint8_t code[TS];
-  long long next_unit;  // this cluster's round-robin cursor (identical in all its CTAs)
 };
 
 constexpr int pow2_floor(int v) { return v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1; }
@@ -92,12 +97,56 @@ struct Geo {
   static constexpr size_t zg_elems = (G > 1 ? (size_t)(G - 1) : 0) * z_elems;
   static constexpr size_t v_elems = (size_t)SL * TS;
   static constexpr size_t r_elems = (size_t)NRB * TS;
-  // a4 | zc | zn | zr | zg | vs | rpart
-  static constexpr size_t smem_bytes = sizeof(T) * (a4_elems + 3 * z_elems + zg_elems + v_elems + r_elems);
+  static constexpr size_t ring_elems = (size_t)RING * SL;
+  static constexpr size_t rall_elems = (size_t)16 * TS;
+  // a4 | zc | zn (= reduced z) | zin (peer partials) | zg | vs | rpart | ring_x | rall
+  static constexpr size_t smem_bytes =
+      sizeof(T) * (a4_elems + 3 * z_elems + zg_elems + v_elems + r_elems + ring_elems + rall_elems);
 };
 
 // swizzled 16-byte chunk of V row `row` holding slots [4c, 4c+3]
 __device__ __forceinline__ int vchunk(int row, int c) { return c ^ ((row >> 2) & 7); }
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(void* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(void* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  } while (!done);
+}
+// 16-byte asynchronous store into a peer CTA's shared memory, completing bytes on its mbarrier
+__device__ __forceinline__ void st_async16(uint32_t peer_dst, const void* src16, uint32_t peer_bar) {
+  const uint4 v = *reinterpret_cast<const uint4*>(src16);
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(peer_dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(peer_bar) : "memory");
+}
+// element-sized asynchronous global->shared copy (zero-filled when !valid)
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool valid) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte elements");
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <typename T, int KP, int SL, int NT>
 __global__ void __launch_bounds__(NT, 1)
@@ -108,12 +157,14 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
   constexpr int QS = Gm::QS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* a4 = reinterpret_cast<T*>(smem_raw);
-  T* zc = a4 + Gm::a4_elems;   // z_it used by phase a                    [KP][TS]
-  T* zn = zc + Gm::z_elems;    // this CTA's partial of z_{it+1}          [KP][TS]
-  T* zr = zn + Gm::z_elems;    // cluster-reduced z_{it+1}                [KP][TS]
-  T* zg = zr + Gm::z_elems;    // phase-c row-group partials (groups 1..) [G-1][KP][TS]
-  T* vs = zg + Gm::zg_elems;   // v, swizzled                             [SL][TS]
-  T* rpart = vs + Gm::v_elems; // per-32-row-block slot max|r|            [NRB][TS]
+  T* zc = a4 + Gm::a4_elems;      // z_it used by phase a                       [KP][TS]
+  T* zn = zc + Gm::z_elems;       // partial of z_{it+1}, then the reduced z    [KP][TS]
+  T* zin = zn + Gm::z_elems;      // peers' partials of this CTA's row slice    [C][KP/C][TS]
+  T* zg = zin + Gm::z_elems;      // phase-c row-group partials (groups 1..)    [G-1][KP][TS]
+  T* vs = zg + Gm::zg_elems;      // v, swizzled                                [SL][TS]
+  T* rpart = vs + Gm::v_elems;    // per-32-row-block slot max|r|               [NRB][TS]
+  T* ring_x = rpart + Gm::r_elems;  // x rows of prefetched units             [RING][SL]
+  T* rall = ring_x + Gm::ring_elems;  // every CTA's slot max|r|              [16][TS]
   __shared__ Slots<T> ss;
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -123,6 +174,7 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row_base = crank * SL;
   const T tol = (T)P.tol, rho = (T)P.rho;
+  const int rs = KP / C;  // rows of z reduced by each CTA
 
   // ---- resident dictionary rows: a4[q][t][r] = A[row_base + 4q + r][t]
   for (int e = tid; e < (int)Gm::a4_elems; e += NT) {
@@ -132,25 +184,40 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
   }
   for (int e = tid; e < (int)Gm::z_elems; e += NT) zc[e] = T(0);
 
-  // ---- phase a / b ownership: rows 4*quad .. +3, slots slot0 .. +3
   const int rb = warp >> 1, sh = warp & 1;
   const int rq = lane >> 2, sq = lane & 3;
   const int quad = rb * 8 + rq;
   const int lrow0 = 4 * quad;
   const int grow0 = row_base + lrow0;
   const int slot0 = sh * 16 + sq * 4;
-  // ---- phase c ownership
   const int kq = lane & 3, sq8 = lane >> 2;
 
-  T xr[4][4], yr[4][4], lr[4][4];  // [row][slot]
+  T xr[4][4], yr[4][4], lr[4][4];  // ADM state [row][slot]
 
-  auto install_unit = [&](int slot, int64_t u) {
-    const T sc = scale[u];
+  // candidate j of this cluster is unit cid + j * nclusters
+  auto cand = [&](long long j) -> long long { return (long long)cid + j * (long long)nclusters; };
+  // all threads: start prefetching candidates [pf_from, pf_to) into the ring
+  auto prefetch = [&]() {
+    for (long long j = ss.pf_from; j < ss.pf_to; ++j) {
+      const int e = (int)(j % RING);
+      const long long u = cand(j);
+      const bool ok = u < P.n_units;
+      for (int r = tid; r < SL; r += NT)
+        cp_async_elem(ring_x + (size_t)e * SL + r, X + (ok ? u : 0) * P.ldx + (ok && row_base + r < P.s ? row_base + r : 0),
+                  ok && row_base + r < P.s);
+      if (tid == 0) {
+        ss.ring_u[e] = u;
+        cp_async_elem(&ss.ring_sc[e], scale + (ok ? u : 0), ok);
+      }
+    }
+  };
+  auto install_unit = [&](int slot, long long u, T sc, int src) {
     const T b0 = P.beta0 > 0 ? (T)P.beta0 : T(1) / sc;
     ss.unit[slot] = (int)u;
     ss.state[slot] = 1;
     ss.it[slot] = 0;
     ss.stalled[slot] = 0;
+    ss.src[slot] = src;
     ss.beta_cur[slot] = b0;
     ss.beta_next[slot] = b0;
     ss.inv_next[slot] = T(1) / b0;
@@ -158,39 +225,69 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
     ss.thresh[slot] = tol * sc;
     ss.prev_res[slot] = Limits<T>::inf();
   };
-  auto claim = [&]() -> int64_t {  // next live unit of this cluster, same in every CTA
+  // one thread: next live unit for `slot` (prefetched ring first, then synchronous)
+  auto claim_into = [&](int slot) {
     for (;;) {
-      const long long u = ss.next_unit;
-      if (u >= P.n_units) return -1;
-      ss.next_unit = u + nclusters;
-      if (scale[u] > T(0)) return u;
+      if (ss.head < ss.tail) {
+        const int e = (int)(ss.head % RING);
+        const long long u = ss.ring_u[e];
+        ss.head++;
+        if (u >= P.n_units) break;
+        if (ss.ring_sc[e] > T(0)) { install_unit(slot, u, ss.ring_sc[e], e); return; }
+      } else {
+        const long long u = cand(ss.head);
+        ss.head++;
+        ss.tail = ss.head;
+        if (u >= P.n_units) break;
+        const T sc = scale[u];
+        if (sc > T(0)) { install_unit(slot, u, sc, -1); return; }
+      }
     }
+    ss.state[slot] = 0;
+    ss.unit[slot] = -1;
   };
   auto load_slot = [&](int j) {  // (re)initialise this thread's state of slot slot0+j
     const int slot = slot0 + j;
     const bool live = ss.state[slot] == 1;
+    const int src = ss.src[slot];
     const int64_t u = live ? ss.unit[slot] : 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int row = grow0 + i;
-      xr[i][j] = (live && row < P.s) ? X[u * P.ldx + row] : T(0);
+      T x = T(0);
+      if (live && row < P.s) x = src >= 0 ? ring_x[(size_t)src * SL + lrow0 + i] : X[u * P.ldx + row];
+      xr[i][j] = x;
       yr[i][j] = T(0);
       lr[i][j] = T(0);
     }
   };
 
   if (tid == 0) {
-    ss.next_unit = cid;
-    for (int sl = 0; sl < TS; ++sl) {
-      const int64_t u = claim();
-      if (u < 0) { ss.state[sl] = 0; ss.unit[sl] = -1; } else install_unit(sl, u);
-      ss.finish[sl] = 0;
-    }
+    ss.head = 0; ss.tail = 0; ss.pf_from = 0; ss.pf_to = RING;
+    mbar_init(&ss.bar_p, 1);
+    mbar_init(&ss.bar_r, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  prefetch();
+  cp_async_wait_all();
+  __syncthreads();
+  if (tid == 0) {
+    ss.tail = RING;
+    for (int sl = 0; sl < TS; ++sl) { claim_into(sl); ss.finish[sl] = 0; }
+    ss.pf_from = ss.tail;
+    ss.pf_to = ss.head + RING;
+    if (ss.pf_to < ss.pf_from) ss.pf_to = ss.pf_from;
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < 4; ++j) load_slot(j);
+  __syncthreads();
+  if (tid == 0) ss.tail = ss.pf_to;
+  prefetch();
+  if (C > 1) cluster.sync();  // peers' mbarriers initialised before any DSMEM traffic
 
+  uint32_t phase = 0;
   for (;;) {
     if (!__syncthreads_or(tid < TS && ss.state[tid] == 1)) break;
 
@@ -248,7 +345,6 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
         }
         az[i][j] = v;
       }
-      // max over the 8 row quads of this warp that share the slot
       m = tmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
       m = tmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
       m = tmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
@@ -300,7 +396,7 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
       T m = T(0);
 #pragma unroll
       for (int b = 0; b < Gm::NRB; ++b) m = tmax(m, rpart[b * TS + tid]);
-      ss.rloc[tid] = m;
+      rall[crank * TS + tid] = m;
     }
     __syncthreads();
     if (Gm::G > 1) {
@@ -310,38 +406,57 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
         for (int g = 1; g < Gm::G; ++g) sacc += zg[(size_t)(g - 1) * Gm::z_elems + e];
         zn[e] = sacc;
       }
-    }
-
-    // ========== cluster reduction of z and max|r|
-    const T* zsum = zn;
-    if (C > 1) {
-      cluster.sync();
-      const int rows_per = KP / C;
-      const int e0 = crank * rows_per * TS, e1 = e0 + rows_per * TS;
-      for (int e = e0 + tid; e < e1; e += NT) {
-        T sacc = T(0);
-        for (int c = 0; c < C; ++c) sacc += cluster.map_shared_rank(zn, c)[e];
-        for (int c = 0; c < C; ++c) cluster.map_shared_rank(zr, c)[e] = sacc;
-      }
-      if (tid < TS) {
-        T m = T(0);
-        for (int c = 0; c < C; ++c) m = tmax(m, cluster.map_shared_rank(&ss.rloc[0], c)[tid]);
-        ss.res[tid] = m;
-      }
-      cluster.sync();
-      zsum = zr;
-    } else {
-      if (tid < TS) ss.res[tid] = ss.rloc[tid];
       __syncthreads();
     }
 
-    // ========== per-slot decision (l1reg.py:100-128), identical in every CTA
-    if (tid < TS) {
-      const int slot = tid;
+    // ========== cluster reduction: partial slices -> owners, reduced slices + max|r| -> all
+    if (C > 1) {
+      constexpr int CH = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+      const int slice_chunks = rs * TS / CH;
+      const uint32_t bar_p = smem_addr(&ss.bar_p), bar_r = smem_addr(&ss.bar_r);
+      if (tid == 0) {
+        mbar_arm(&ss.bar_p, (uint32_t)((C - 1) * rs * TS * sizeof(T)));
+        mbar_arm(&ss.bar_r, (uint32_t)((C - 1) * (rs * TS + TS) * sizeof(T)));
+      }
+      // my partial of owner c's slice -> zin[crank] of owner c
+      for (int idx = tid; idx < (C - 1) * slice_chunks; idx += NT) {
+        const int d = idx / slice_chunks, ch = idx - d * slice_chunks;
+        const int owner = d < crank ? d : d + 1;
+        const T* src = zn + (size_t)owner * rs * TS + (size_t)ch * CH;
+        const uint32_t dst = peer_addr(smem_addr(zin + (size_t)crank * rs * TS + (size_t)ch * CH), owner);
+        st_async16(dst, src, peer_addr(bar_p, owner));
+      }
+      mbar_wait(&ss.bar_p, phase);
+      // reduce my slice in rank order, then push it (and my max|r|) to every peer
+      T* mine = zn + (size_t)crank * rs * TS;
+      for (int e = tid; e < rs * TS; e += NT) {
+        T sacc = T(0);
+        for (int c = 0; c < C; ++c) sacc += (c == crank) ? mine[e] : zin[(size_t)c * rs * TS + e];
+        mine[e] = sacc;
+      }
+      __syncthreads();
+      const int push_chunks = slice_chunks + TS / CH;
+      for (int idx = tid; idx < (C - 1) * push_chunks; idx += NT) {
+        const int d = idx / push_chunks, ch = idx - d * push_chunks;
+        const int peer = d < crank ? d : d + 1;
+        // same offset in the peer: my reduced slice of z, then my slot max|r|
+        const T* src = ch < slice_chunks ? mine + (size_t)ch * CH : rall + (size_t)crank * TS + (size_t)(ch - slice_chunks) * CH;
+        st_async16(peer_addr(smem_addr(src), peer), src, peer_addr(bar_r, peer));
+      }
+      mbar_wait(&ss.bar_r, phase);
+      phase ^= 1;
+    }
+
+    // ========== decision, outputs and refill claims: warp 0 (identical in every CTA)
+    cp_async_wait_all();
+    if (warp == 0) {
+      const int slot = lane;
       bool fin = false;
+      T r = T(0);
+      for (int c = 0; c < C; ++c) r = tmax(r, rall[c * TS + slot]);
+      ss.res[slot] = r;
       if (ss.state[slot] == 1) {
         if (ss.it[slot] > 0) {
-          const T r = ss.res[slot];
           const T prev = ss.prev_res[slot];
           const T rel = tabs(r - prev) / tmax(r, Limits<T>::tiny());
           ss.stalled[slot] = (rel < (T)kStallEps) ? ss.stalled[slot] + 1 : 0;
@@ -361,41 +476,41 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
         }
       }
       ss.finish[slot] = fin;
-    }
-    __syncthreads();
-
-    // ========== outputs of finished units (z_it is still in zc)
-    if (crank == 0) {
-      for (int slot = warp; slot < TS; slot += Gm::NW) {
-        if (!ss.finish[slot]) continue;
-        const int64_t u = ss.unit[slot];
-        for (int t = lane; t < P.k; t += 32) Z[u * P.ldz + t] = zc[t * TS + slot];
-        if (lane == 0) {
-          if (iters) iters[u] = ss.it[slot];
-          if (res_out) res_out[u] = ss.res[slot];
-          if (status) status[u] = ss.code[slot];
+      unsigned fmask = __ballot_sync(0xffffffffu, fin);
+      if (crank == 0) {  // outputs of finished units: z_it is still in zc
+        for (unsigned mm = fmask; mm; mm &= mm - 1) {
+          const int sl = __ffs(mm) - 1;
+          const int64_t u = ss.unit[sl];
+          for (int t = lane; t < P.k; t += 32) Z[u * P.ldz + t] = zc[t * TS + sl];
+          if (lane == 0) {
+            if (iters) iters[u] = ss.it[sl];
+            if (res_out) res_out[u] = ss.res[sl];
+            if (status) status[u] = ss.code[sl];
+          }
         }
       }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int slot = 0; slot < TS; ++slot) {
-        if (!ss.finish[slot]) continue;
-        const int64_t u = claim();
-        if (u < 0) { ss.state[slot] = 0; ss.unit[slot] = -1; } else install_unit(slot, u);
+      __syncwarp();
+      if (lane == 0) {
+        for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
+        ss.pf_from = ss.tail > ss.head ? ss.tail : ss.head;
+        if (ss.tail < ss.head) ss.tail = ss.head;
+        ss.pf_to = ss.head + RING;
+        ss.tail = ss.pf_to;
       }
     }
     __syncthreads();
     // ========== install z_{it+1} (zero for fresh / empty slots), reload refilled slots
+    const T* zsum = zn;
     for (int e = tid; e < (int)Gm::z_elems; e += NT) {
       const int slot = e % TS;
       zc[e] = (ss.state[slot] == 1 && ss.it[slot] > 0) ? zsum[e] : T(0);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (ss.finish[slot0 + j]) load_slot(j);  // finish[] is rewritten by every decision step
+      if (ss.finish[slot0 + j]) load_slot(j);
+    __syncthreads();  // ring entries consumed by load_slot before they are refilled
+    prefetch();
   }
-  // keep every CTA's shared memory alive until its cluster peers are done with it
   if (C > 1) cluster.sync();
 }
 
