@@ -92,6 +92,7 @@ struct Geo {
   static_assert(KP % 16 == 0, "KP must be a multiple of 16");
   static_assert(NW == NRB * 2, "phase a: one warp per (32-row block, 16-slot half)");
   static_assert(QUADS % G == 0, "row groups must split the quads evenly");
+  static_assert((QUADS / G) % 8 == 0, "phase c walks quads in blocks of 8");
   static constexpr size_t a4_elems = (size_t)QUADS * QS * 4;
   static constexpr size_t z_elems = (size_t)KP * TS;
   static constexpr size_t zg_elems = (G > 1 ? (size_t)(G - 1) : 0) * z_elems;
@@ -125,7 +126,7 @@ __device__ __forceinline__ void mbar_wait(void* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done) : "r"(a), "r"(parity) : "memory");
   } while (!done);
 }
@@ -288,10 +289,64 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
   if (C > 1) cluster.sync();  // peers' mbarriers initialised before any DSMEM traffic
 
   uint32_t phase = 0;
+  T* zcur = zc;   // z_it read by phase a
+  T* znext = zn;  // partial, then reduced, z_{it+1}
+  T* zprev = zn;  // z of the previous pass (outputs of units finishing there)
+  bool first = true;
   for (;;) {
-    if (!__syncthreads_or(tid < TS && ss.state[tid] == 1)) break;
+    // ========== warp 0: decision of the previous pass, outputs, refill claims
+    //            (overlaps the other warps' phase a; identical in every CTA)
+    if (warp == 0 && !first) {
+      const int slot = lane;
+      bool fin = false;
+      T r = T(0);
+      for (int c = 0; c < C; ++c) r = tmax(r, rall[c * TS + slot]);
+      if (ss.state[slot] == 1) {
+        if (ss.it[slot] > 0) {
+          const T prev = ss.prev_res[slot];
+          const T rel = tabs(r - prev) / tmax(r, Limits<T>::tiny());
+          ss.stalled[slot] = (rel < (T)kStallEps) ? ss.stalled[slot] + 1 : 0;
+          ss.prev_res[slot] = r;
+          if (r <= ss.thresh[slot]) { fin = true; ss.code[slot] = L1F_UNIT_OK; }
+          else if (ss.stalled[slot] >= kStallIters) { fin = true; ss.code[slot] = L1F_UNIT_STALLED; }
+          else if (ss.it[slot] >= P.max_iter) { fin = true; ss.code[slot] = L1F_UNIT_MAXITER; }
+        }
+        if (!fin) {
+          ss.it[slot] += 1;
+          const T bc = ss.beta_next[slot];
+          ss.beta_cur[slot] = bc;
+          T bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
+          if (bn > ss.beta_max[slot]) bn = ss.beta_max[slot];
+          ss.beta_next[slot] = bn;
+          ss.inv_next[slot] = T(1) / bn;
+        }
+      }
+      ss.res[slot] = r;
+      ss.finish[slot] = fin;
+      const unsigned fmask = __ballot_sync(0xffffffffu, fin);
+      if (crank == 0) {  // outputs: the finished iteration's z is in zprev
+        for (unsigned mm = fmask; mm; mm &= mm - 1) {
+          const int sl = __ffs(mm) - 1;
+          const int64_t u = ss.unit[sl];
+          for (int t = lane; t < P.k; t += 32) Z[u * P.ldz + t] = zprev[t * TS + sl];
+          if (lane == 0) {
+            if (iters) iters[u] = ss.it[sl];
+            if (res_out) res_out[u] = ss.res[sl];
+            if (status) status[u] = ss.code[sl];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
+        ss.pf_from = ss.tail > ss.head ? ss.tail : ss.head;
+        ss.pf_to = ss.head + RING;
+        ss.tail = ss.pf_to;
+      }
+      __syncwarp();
+    }
 
-    // ========== phase a: az[i][j] = sum_t A[row i][t] z_it[t][slot j]
+    // ========== phase a: az[i][j] = sum_t A[row i][t] z_it[t][slot j]  (software pipelined)
     T az[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -299,19 +354,37 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
       for (int j = 0; j < 4; ++j) az[i][j] = T(0);
     {
       const T* acell = a4 + (size_t)quad * QS * 4;
-      const T* zrow = zc + slot0;
-      const int ka = P.ka;
-#pragma unroll 4
-      for (int t = 0; t < ka; ++t) {
-        T a[4], z[4];
-        Vec4<T>::ld(acell + 4 * t, a);
-        Vec4<T>::ld(zrow + t * TS, z);
+      const T* zrow = zcur + slot0;
+      const int ka = P.ka;  // multiple of 4
+      T a0[4], z0[4], a1[4], z1[4];
+      Vec4<T>::ld(acell, a0);
+      Vec4<T>::ld(zrow, z0);
+      Vec4<T>::ld(acell + 4, a1);
+      Vec4<T>::ld(zrow + TS, z1);
+      for (int t = 0; t < ka; t += 2) {
+        T na0[4], nz0[4], na1[4], nz1[4];
+        const int tn = t + 2 < ka ? t + 2 : t;  // harmless reload on the last step
+        Vec4<T>::ld(acell + 4 * tn, na0);
+        Vec4<T>::ld(zrow + tn * TS, nz0);
+        Vec4<T>::ld(acell + 4 * tn + 4, na1);
+        Vec4<T>::ld(zrow + (tn + 1) * TS, nz1);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) az[i][j] = fma(a[i], z[j], az[i][j]);
+          for (int j = 0; j < 4; ++j) az[i][j] = fma(a0[i], z0[j], az[i][j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) az[i][j] = fma(a1[i], z1[j], az[i][j]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { a0[q] = na0[q]; z0[q] = nz0[q]; a1[q] = na1[q]; z1[q] = nz1[q]; }
       }
     }
+    if (!__syncthreads_or(tid < TS && ss.state[tid] == 1)) break;
+    first = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ss.finish[slot0 + j]) load_slot(j);
 
     // ========== phase b: elementwise ADM update (reformulated residual), v -> shared
 #pragma unroll
@@ -357,8 +430,9 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
       Vec4<T>::st(vs + (size_t)row * TS + 4 * vchunk(row, slot0 >> 2), v4);
     }
     __syncthreads();
+    prefetch();  // ring entries claimed above were consumed by load_slot
 
-    // ========== phase c: z_part[k][slot] = sum_rows A[row][k] v[row][slot]
+    // ========== phase c: z_part[k][slot] = sum_rows A[row][k] v[row][slot]  (pipelined)
 #pragma unroll
     for (int ii = 0; ii < Gm::IPW; ++ii) {
       const int item = warp + ii * Gm::NW;
@@ -370,24 +444,28 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2) acc[j][s2] = T(0);
         const int kbase = kt * 16 + kq;
-        const int q0 = g * Gm::QPG;
-#pragma unroll 2
-        for (int q = q0; q < q0 + Gm::QPG; ++q) {
-          T a[4][4];  // [k j][row r]
+        const int q0 = g * Gm::QPG, q1 = q0 + Gm::QPG;
+        // quads in blocks of 8: (q & 7) == qq is compile-time, so is the V swizzle
+        for (int qb = q0; qb < q1; qb += 8) {
+          const T* acell = a4 + ((size_t)qb * QS + kbase) * 4;
+          const T* vblk = vs + (size_t)(4 * qb) * TS;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) Vec4<T>::ld(a4 + ((size_t)q * QS + kbase + 4 * j) * 4, a[j]);
+          for (int qq = 0; qq < 8; ++qq) {
+            T a[4][4];  // [k j][row r]
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = 4 * q + r;
-            T v[4];
-            Vec4<T>::ld(vs + (size_t)row * TS + 4 * vchunk(row, sq8), v);
+            for (int j = 0; j < 4; ++j) Vec4<T>::ld(acell + ((size_t)qq * QS + 4 * j) * 4, a[j]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int r = 0; r < 4; ++r) {
+              T v[4];
+              Vec4<T>::ld(vblk + (size_t)(4 * qq + r) * TS + 4 * (sq8 ^ qq), v);
 #pragma unroll
-              for (int s2 = 0; s2 < 4; ++s2) acc[j][s2] = fma(a[j][r], v[s2], acc[j][s2]);
+              for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) acc[j][s2] = fma(a[j][r], v[s2], acc[j][s2]);
+            }
           }
         }
-        T* dst = (g == 0) ? zn : zg + (size_t)(g - 1) * Gm::z_elems;
+        T* dst = (g == 0) ? znext : zg + (size_t)(g - 1) * Gm::z_elems;
 #pragma unroll
         for (int j = 0; j < 4; ++j) Vec4<T>::st(dst + (size_t)(kbase + 4 * j) * TS + 4 * sq8, acc[j]);
       }
@@ -401,12 +479,12 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
     __syncthreads();
     if (Gm::G > 1) {
       for (int e = tid; e < (int)Gm::z_elems; e += NT) {
-        T sacc = zn[e];
+        T sacc = znext[e];
 #pragma unroll
         for (int g = 1; g < Gm::G; ++g) sacc += zg[(size_t)(g - 1) * Gm::z_elems + e];
-        zn[e] = sacc;
+        znext[e] = sacc;
       }
-      __syncthreads();
+      if (C > 1) __syncthreads();
     }
 
     // ========== cluster reduction: partial slices -> owners, reduced slices + max|r| -> all
@@ -418,17 +496,15 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
         mbar_arm(&ss.bar_p, (uint32_t)((C - 1) * rs * TS * sizeof(T)));
         mbar_arm(&ss.bar_r, (uint32_t)((C - 1) * (rs * TS + TS) * sizeof(T)));
       }
-      // my partial of owner c's slice -> zin[crank] of owner c
       for (int idx = tid; idx < (C - 1) * slice_chunks; idx += NT) {
         const int d = idx / slice_chunks, ch = idx - d * slice_chunks;
         const int owner = d < crank ? d : d + 1;
-        const T* src = zn + (size_t)owner * rs * TS + (size_t)ch * CH;
+        const T* src = znext + (size_t)owner * rs * TS + (size_t)ch * CH;
         const uint32_t dst = peer_addr(smem_addr(zin + (size_t)crank * rs * TS + (size_t)ch * CH), owner);
         st_async16(dst, src, peer_addr(bar_p, owner));
       }
       mbar_wait(&ss.bar_p, phase);
-      // reduce my slice in rank order, then push it (and my max|r|) to every peer
-      T* mine = zn + (size_t)crank * rs * TS;
+      T* mine = znext + (size_t)crank * rs * TS;
       for (int e = tid; e < rs * TS; e += NT) {
         T sacc = T(0);
         for (int c = 0; c < C; ++c) sacc += (c == crank) ? mine[e] : zin[(size_t)c * rs * TS + e];
@@ -445,71 +521,14 @@ adm_resident_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t ld
       }
       mbar_wait(&ss.bar_r, phase);
       phase ^= 1;
+    } else if (Gm::G > 1) {
+      __syncthreads();
     }
-
-    // ========== decision, outputs and refill claims: warp 0 (identical in every CTA)
     cp_async_wait_all();
-    if (warp == 0) {
-      const int slot = lane;
-      bool fin = false;
-      T r = T(0);
-      for (int c = 0; c < C; ++c) r = tmax(r, rall[c * TS + slot]);
-      ss.res[slot] = r;
-      if (ss.state[slot] == 1) {
-        if (ss.it[slot] > 0) {
-          const T prev = ss.prev_res[slot];
-          const T rel = tabs(r - prev) / tmax(r, Limits<T>::tiny());
-          ss.stalled[slot] = (rel < (T)kStallEps) ? ss.stalled[slot] + 1 : 0;
-          ss.prev_res[slot] = r;
-          if (r <= ss.thresh[slot]) { fin = true; ss.code[slot] = L1F_UNIT_OK; }
-          else if (ss.stalled[slot] >= kStallIters) { fin = true; ss.code[slot] = L1F_UNIT_STALLED; }
-          else if (ss.it[slot] >= P.max_iter) { fin = true; ss.code[slot] = L1F_UNIT_MAXITER; }
-        }
-        if (!fin) {
-          ss.it[slot] += 1;
-          const T bc = ss.beta_next[slot];
-          ss.beta_cur[slot] = bc;
-          T bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
-          if (bn > ss.beta_max[slot]) bn = ss.beta_max[slot];
-          ss.beta_next[slot] = bn;
-          ss.inv_next[slot] = T(1) / bn;
-        }
-      }
-      ss.finish[slot] = fin;
-      unsigned fmask = __ballot_sync(0xffffffffu, fin);
-      if (crank == 0) {  // outputs of finished units: z_it is still in zc
-        for (unsigned mm = fmask; mm; mm &= mm - 1) {
-          const int sl = __ffs(mm) - 1;
-          const int64_t u = ss.unit[sl];
-          for (int t = lane; t < P.k; t += 32) Z[u * P.ldz + t] = zc[t * TS + sl];
-          if (lane == 0) {
-            if (iters) iters[u] = ss.it[sl];
-            if (res_out) res_out[u] = ss.res[sl];
-            if (status) status[u] = ss.code[sl];
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
-        ss.pf_from = ss.tail > ss.head ? ss.tail : ss.head;
-        if (ss.tail < ss.head) ss.tail = ss.head;
-        ss.pf_to = ss.head + RING;
-        ss.tail = ss.pf_to;
-      }
-    }
-    __syncthreads();
-    // ========== install z_{it+1} (zero for fresh / empty slots), reload refilled slots
-    const T* zsum = zn;
-    for (int e = tid; e < (int)Gm::z_elems; e += NT) {
-      const int slot = e % TS;
-      zc[e] = (ss.state[slot] == 1 && ss.it[slot] > 0) ? zsum[e] : T(0);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (ss.finish[slot0 + j]) load_slot(j);
-    __syncthreads();  // ring entries consumed by load_slot before they are refilled
-    prefetch();
+    __syncthreads();  // reduced z, rall and the prefetched ring visible to warp 0
+    zprev = zcur;
+    zcur = znext;
+    znext = zprev;
   }
   if (C > 1) cluster.sync();
 }
