@@ -212,3 +212,30 @@ def test_rank_estimation_and_cross_validation():
     sol = l1pcp.estimate_rank_and_solve(m, l1pcp.FilterConfig(rng_seed=0, cross_validate=True))
     assert sol.method == "l1-filter" and sol.rank_of_l == 3
     assert l1pcp.rel_err(sol.l, l0) <= 1e-5
+
+
+def test_sharded_cuda_backend_matches_single_gpu_solve():
+    """distributed.solve_sharded with the production CudaBackend (NCCL, world size 1) gives the
+    same L/S as the single-GPU engine on the same seed indices."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_1108_5359_b200 import distributed as pdist
+
+    mt, _, _, _ = engine.generate_matrix(600, 500, 5, 0.05, 500.0, seed=2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ri, ci = engine.sample_indices(600, 500, 50, 50, np.random.SeedSequence(0).spawn(1)[0])
+        plan = pdist.ShardPlan(600, 500, 0, 1, ri, ci)
+        adm = l1pcp.AdmConfig(tol=1e-7)
+        l, s, info = pdist.solve_sharded(mt, plan, pdist.CudaBackend(), adm)
+    finally:
+        dist.destroy_process_group()
+    sol = l1pcp.estimate_rank_and_solve(mt, l1pcp.FilterConfig(rank_hint=5, rng_seed=0, adm=adm))
+    assert info["k"] == sol.rank_of_l == 5
+    assert torch.equal(l, sol.l) and torch.equal(s, sol.s)
