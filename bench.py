@@ -266,8 +266,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step(evs=None):
-        from paper_1108_5359_b200 import _device as dv  # noqa: F401
-        f = engine.filter_stage(plan, mt) if evs is None else _staged(plan, mt, evs)
+        f = engine.filter_stage(plan, mt, evs)
         af, bf = engine.build_factors(plan, f["zc"], f["zr"])
         if evs is not None:
             evs[3].record(stream)
@@ -338,6 +337,7 @@ def run_ours(args):
         "data": "synthetic (Philox4x64-10 on device; BASELINE.json config statistics)",
         "config": {"workload": workload_name(cfgd), "m": m, "n": n, "rank": r, "seed_block": [s_r, s_c],
                    "r_prime": k, "tol": TOL, "parallelism": "1 GPU",
+                   "filter_dtype": "f64" if plan.filter_dtype == torch.float64 else "f32",
                    "l2": "inputs larger than L2 (M is %.1f GB)" % (m * n * 4 / 1e9)},
         "roofline": {"bound": "fp32", "kernel": "adm_filter_kernel (column + row filters)", "achieved": achieved,
                      "peak": fma_tflops, "unit": "TFLOP/s", "frac": achieved / fma_tflops,
@@ -362,28 +362,6 @@ def run_ours(args):
     }
     print(json.dumps(line))
     return 0
-
-
-def _staged(plan, mt, evs):
-    """filter_stage with events: evs[0] start, evs[1] after gathers, evs[2] after filters."""
-    import torch
-    from paper_1108_5359_b200 import _device as dv, _lib
-    from paper_1108_5359_b200.l1reg import filter_units
-    stream = torch.cuda.current_stream()
-    evs[0].record(stream)
-    xc = torch.empty((len(plan.comp_cols), len(plan.seed.row_idx)), dtype=mt.dtype, device="cuda")
-    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx),
-              len(plan.seed.row_idx), dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt), dv.ptr(xc),
-              xc.stride(0), 1, dv.stream())
-    xr = torch.empty((len(plan.comp_rows), len(plan.seed.col_idx)), dtype=mt.dtype, device="cuda")
-    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local),
-              len(plan.comp_rows), dv.ptr(plan.d_col_idx), len(plan.seed.col_idx), dv.dtype_code(mt), dv.ptr(xr),
-              xr.stride(0), 0, dv.stream())
-    evs[1].record(stream)
-    zc, _, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=False, workspace=plan.workspace)
-    zr, _, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=False, workspace=plan.workspace)
-    evs[2].record(stream)
-    return dict(zc=zc, zr=zr, iters_c=itc, iters_r=itr, status_c=stc, status_r=st_r)
 
 
 def run_e2e(mt, plan, args, l_dev, s_dev):

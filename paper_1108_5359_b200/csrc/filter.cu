@@ -431,16 +431,25 @@ int l1f_resident_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const
                           T* E, int64_t lde, int32_t* iters, T* res, uint8_t* status, void* workspace,
                           size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
 
+template <typename T>
+int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
+                       double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
+                       int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
+                       bool query, size_t* need);
+
 namespace l1f {
 namespace filt {
 
-// resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
+// small-k group kernel (filter_small.cu), resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
 template <typename T>
 int select(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
            double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
            int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
            bool query, size_t* need) {
   if (!force_streaming()) {
+    const int rs = l1f_small_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz,
+                                         E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
+    if (rs != L1F_ERR_UNSUPPORTED) return rs;
     const int rc = l1f_resident_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z,
                                             ldz, E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
     if (rc != L1F_ERR_UNSUPPORTED) return rc;

@@ -170,8 +170,9 @@ class CudaBackend:
 
     def filter(self, x_um, a64, adm):
         from .l1reg import filter_units
-        z, _, it, _, st = filter_units(x_um, a64.to(x_um.dtype).contiguous(), adm, want_e=False)
-        return z, it, st
+        fdt = self.engine.filter_dtype_for(a64.shape[1], x_um.dtype)  # same rule as the 1-GPU engine
+        z, _, it, _, st = filter_units(x_um.to(fdt).contiguous(), a64.to(fdt).contiguous(), adm, want_e=False)
+        return z.to(x_um.dtype), it, st
 
     def reconstruct(self, m_local, plan, u, sig, v, zc_all, zr):
         seed = self.engine.DeviceSeed(row_idx=plan.row_idx, col_idx=plan.col_idx, u=u, sigma=sig, v=v, seed_l=None,

@@ -153,14 +153,24 @@ def seed_stage(mt, cfg):
         r = max(r_prime, r + 1)  # undersized seed, l1filter.py:237
 
 
+# ranks up to this use the small-k group kernel in FP64: at tol 1e-7 an FP32 residual cannot
+# always resolve tol * ||x||_inf when the largest entries are uncorrupted (video data, config 4)
+SMALL_K_FP64 = 16
+
+
+def filter_dtype_for(k, dtype):
+    return torch.float64 if k <= SMALL_K_FP64 else dtype
+
+
 class FilterPlan:
     """Everything the timed solve needs that does not depend on M's values: index sets on
-    the device, seed factors cast to the working dtype, workspaces and output buffers."""
+    the device, seed factors cast to the filter dtype, workspaces and output buffers."""
 
     def __init__(self, m_rows, m_cols, seed, dtype, adm, want_e=False, row_range=None, col_units=None):
         self.m_rows, self.m_cols = m_rows, m_cols
         self.seed = seed
         self.dtype = dtype
+        self.filter_dtype = filter_dtype_for(seed.r_prime, dtype)
         self.adm = adm
         self.want_e = want_e
         self.k = seed.r_prime
@@ -176,44 +186,45 @@ class FilterPlan:
         self.d_col_idx = index_tensor(seed.col_idx)
         self.d_comp_cols = index_tensor(self.comp_cols)
         self.d_comp_rows_local = index_tensor(self.comp_rows - r0)
-        self.u = seed.u.to(dtype).contiguous()
-        self.v = seed.v.to(dtype).contiguous()
-        code = _lib.F32 if dtype == torch.float32 else _lib.F64
+        self.u = seed.u.to(self.filter_dtype).contiguous()
+        self.v = seed.v.to(self.filter_dtype).contiguous()
+        code = _lib.F32 if self.filter_dtype == torch.float32 else _lib.F64
         s_r, s_c = len(seed.row_idx), len(seed.col_idx)
         nbytes = max(_lib.load().l1f_filter_workspace_bytes(code, s_r, self.k, len(self.comp_cols)),
                      _lib.load().l1f_filter_workspace_bytes(code, s_c, self.k, len(self.comp_rows)))
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
 
 
-def filter_stage(plan, mt, seed_rows=None):
+def filter_stage(plan, mt, events=None):
     """Column and row filtering (l1filter.py:239-248) for the units of ``plan``.
 
-    mt: the (local rows of the) matrix; seed_rows: optional (s_r, n) tensor holding
-    M[row_idx, :] when mt does not contain all seed rows (row-sharded runs).
-    Returns dict(zc, zr, ec, er, iters_c, iters_r, status_c, status_r).
+    events: optional [start, after_gathers, after_filters] CUDA events recorded on the
+    current stream.  Returns dict(zc, zr, iters_c, iters_r, res_c, res_r, status_c, status_r)
+    with zc / zr in M's dtype.
     """
     from .l1reg import filter_units
-    r0 = plan.row_range[0]
-    if seed_rows is None:
-        # column panel M[row_idx, comp_cols], unit-major (one column unit per row)
-        xc = torch.empty((len(plan.comp_cols), len(plan.seed.row_idx)), dtype=mt.dtype, device="cuda")
-        _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx),
-                  len(plan.seed.row_idx), dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt),
-                  dv.ptr(xc), xc.stride(0), 1, dv.stream())
-    else:
-        xc = torch.empty((len(plan.comp_cols), seed_rows.shape[0]), dtype=mt.dtype, device="cuda")
-        _lib.call("l1f_gather", dv.dtype_code(seed_rows), dv.ptr(seed_rows), seed_rows.stride(0), None,
-                  seed_rows.shape[0], dv.ptr(plan.d_comp_cols), len(plan.comp_cols), dv.dtype_code(mt),
-                  dv.ptr(xc), xc.stride(0), 1, dv.stream())
+    fdt = plan.filter_dtype
+    code_in, code_f = dv.dtype_code(mt), (_lib.F32 if fdt == torch.float32 else _lib.F64)
+    stream = torch.cuda.current_stream()
+    if events is not None:
+        events[0].record(stream)
+    # column panel M[row_idx, comp_cols], unit-major (one column unit per row)
+    xc = torch.empty((len(plan.comp_cols), len(plan.seed.row_idx)), dtype=fdt, device="cuda")
+    _lib.call("l1f_gather", code_in, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx), len(plan.seed.row_idx),
+              dv.ptr(plan.d_comp_cols), len(plan.comp_cols), code_f, dv.ptr(xc), xc.stride(0), 1, dv.stream())
     # row panel M[comp_rows, col_idx] (already unit-major)
-    xr = torch.empty((len(plan.comp_rows), len(plan.seed.col_idx)), dtype=mt.dtype, device="cuda")
-    _lib.call("l1f_gather", dv.dtype_code(mt), dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local),
-              len(plan.comp_rows), dv.ptr(plan.d_col_idx), len(plan.seed.col_idx), dv.dtype_code(mt),
-              dv.ptr(xr), xr.stride(0), 0, dv.stream())
+    xr = torch.empty((len(plan.comp_rows), len(plan.seed.col_idx)), dtype=fdt, device="cuda")
+    _lib.call("l1f_gather", code_in, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local), len(plan.comp_rows),
+              dv.ptr(plan.d_col_idx), len(plan.seed.col_idx), code_f, dv.ptr(xr), xr.stride(0), 0, dv.stream())
+    if events is not None:
+        events[1].record(stream)
     ws = plan.workspace
     zc, ec, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=plan.want_e, workspace=ws)
     zr, er, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=plan.want_e, workspace=ws)
-    del r0
+    if events is not None:
+        events[2].record(stream)
+    if fdt != mt.dtype:
+        zc, zr = zc.to(mt.dtype), zr.to(mt.dtype)
     return dict(zc=zc, zr=zr, ec=ec, er=er, iters_c=itc, iters_r=itr, res_c=rc, res_r=rr, status_c=stc,
                 status_r=st_r)
 

@@ -33,7 +33,7 @@ def test_library_version_and_error_string():
 
 def test_workspace_query_needs_no_device():
     n = _lib.load().l1f_filter_workspace_bytes(_lib.F32, 1000, 100, 19000)
-    assert n > 1000 * 128 * 4
+    assert n >= 19000 * 4  # at least the per-unit scale array
     assert _lib.load().l1f_filter_workspace_bytes(_lib.F32, 0, 10, 10) == 0
 
 
