@@ -135,33 +135,144 @@ reconstruct_kernel(int64_t m, int64_t n, int k, const T* __restrict__ Af, int64_
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
   double r2 = 0.0, m2 = 0.0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = r0 + tile_row(ty, i);
-    if (r >= m) continue;
+  for (int h = 0; h < 2; ++h) {  // two halves of 4 rows: 8 x 16-byte loads of M in flight
+    T mv[4][2][4];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const int64_t c = c0 + 4 * tx + 64 * g;
-      T l[4];
+    for (int ii = 0; ii < 4; ++ii) {
+      const int64_t r = r0 + tile_row(ty, 4 * h + ii);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = acc[i][4 * g + q];
-      if (L) store4(L + r * ldl, c, n, l);
-      if (M) {
-        T mv[4], sv[4];
-        load4(M + r * ldm, c, n, mv);
+      for (int g = 0; g < 2; ++g) {
+        if (M && r < m) load4(M + r * ldm, c0 + 4 * tx + 64 * g, n, mv[ii][g]);
+        else
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          sv[q] = mv[q] - l[q];
-          const double d = (double)((mv[q] - l[q]) - sv[q]);
-          r2 += d * d;
-          m2 += (double)mv[q] * (double)mv[q];
+          for (int q = 0; q < 4; ++q) mv[ii][g][q] = T(0);
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int i = 4 * h + ii;
+      const int64_t r = r0 + tile_row(ty, i);
+      if (r >= m) continue;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int64_t c = c0 + 4 * tx + 64 * g;
+        T l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) l[q] = acc[i][4 * g + q];
+        if (L) store4(L + r * ldl, c, n, l);
+        if (M) {
+          T sv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sv[q] = mv[ii][g][q] - l[q];
+            const double d = (double)((mv[ii][g][q] - l[q]) - sv[q]);
+            r2 += d * d;
+            m2 += (double)mv[ii][g][q] * (double)mv[ii][g][q];
+          }
+          if (S) store4(S + r * lds, c, n, sv);
         }
-        if (S) store4(S + r * lds, c, n, sv);
       }
     }
   }
   if (part) {
     const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
     block_sum2(r2, m2, &part[2 * b], &part[2 * b + 1]);
+  }
+}
+
+// ---------------------------------------------------------------- streaming reconstruction (k <= 16)
+// HBM-bound form for small k: CTA tile 64 rows x 128 columns; thread (tr, tc) owns 8 rows x 4
+// consecutive columns, keeps Bf of its 4 columns in registers, reads Af rows from shared memory
+// (warp-uniform -> broadcast), issues all 8 row loads of M before computing, and writes L and S
+// with 16-byte streaming stores.  12 B of DRAM traffic per entry, k FMAs.
+template <typename T> struct Vec4g;
+template <> struct Vec4g<float> {
+  __device__ static __forceinline__ void ld(const float* p, float (&v)[4]) {
+    float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+  __device__ static __forceinline__ void st(float* p, const float (&v)[4]) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  }
+};
+template <> struct Vec4g<double> {
+  __device__ static __forceinline__ void ld(const double* p, double (&v)[4]) {
+    double2 a = __ldcs(reinterpret_cast<const double2*>(p)), b = __ldcs(reinterpret_cast<const double2*>(p + 2));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  __device__ static __forceinline__ void st(double* p, const double (&v)[4]) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    __stcs(reinterpret_cast<double2*>(p + 2), make_double2(v[2], v[3]));
+  }
+};
+
+template <typename T, int KM>
+__global__ void __launch_bounds__(256)
+reconstruct_stream_kernel(int64_t m, int64_t n, int k, const T* __restrict__ Af, int64_t ldaf,
+                          const T* __restrict__ Bf, int64_t ldbf, const T* __restrict__ M, int64_t ldm,
+                          T* __restrict__ L, int64_t ldl, T* __restrict__ S, int64_t lds, double* __restrict__ part,
+                          bool vec) {
+  constexpr int TR = 64, TC = 128, RPT = 8;
+  __shared__ T as[TR][KM + 1];
+  const int tid = threadIdx.x, tc = tid % 32, tr = tid / 32;
+  const int64_t r0 = (int64_t)blockIdx.y * TR, c0 = (int64_t)blockIdx.x * TC + 4 * tc;
+  for (int e = tid; e < TR * KM; e += 256) {
+    const int r = e / KM, t = e % KM;
+    as[r][t] = (r0 + r < m && t < k) ? Af[(r0 + r) * ldaf + t] : T(0);
+  }
+  T b[4][KM];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int t = 0; t < KM; ++t) b[q][t] = (c0 + q < n && t < k) ? Bf[(c0 + q) * ldbf + t] : T(0);
+  __syncthreads();
+  double r2 = 0.0, m2 = 0.0;
+  T mv[RPT][4];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {  // all loads first: 8 x 16 B in flight per thread
+    const int64_t r = r0 + tr * RPT + i;
+    if (r < m && M) {
+      if (vec && c0 + 3 < n) Vec4g<T>::ld(M + r * ldm + c0, mv[i]);
+      else
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mv[i][q] = c0 + q < n ? M[r * ldm + c0 + q] : T(0);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int ri = tr * RPT + i;
+    const int64_t r = r0 + ri;
+    if (r >= m) break;
+    T l[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+    for (int t = 0; t < KM; ++t) {
+      const T a = as[ri][t];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) l[q] = fma(a, b[q][t], l[q]);
+    }
+    T sv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sv[q] = mv[i][q] - l[q];
+      const double d = (double)((mv[i][q] - l[q]) - sv[q]);
+      r2 += d * d;
+      m2 += (double)mv[i][q] * (double)mv[i][q];
+    }
+    if (vec && c0 + 3 < n) {
+      if (L) Vec4g<T>::st(L + r * ldl + c0, l);
+      if (M && S) Vec4g<T>::st(S + r * lds + c0, sv);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c0 + q < n) {
+          if (L) L[r * ldl + c0 + q] = l[q];
+          if (M && S) S[r * lds + c0 + q] = sv[q];
+        }
+    }
+  }
+  if (part) {
+    const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    block_sum2(r2, m2, &part[2 * blk], &part[2 * blk + 1]);
   }
 }
 
@@ -409,20 +520,39 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
   cudaStream_t st = (cudaStream_t)stream;
   if (resid_sq) L1F_CUDA_TRY(cudaMemsetAsync(resid_sq, 0, 2 * sizeof(double), st));
   if (m == 0 || n == 0) return L1F_OK;
-  dim3 grid((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(m, kTile));
+  const bool small = k <= 16;
+  dim3 grid = small ? dim3((unsigned)ceil_div(n, 128), (unsigned)ceil_div(m, 64))
+                    : dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(m, kTile));
   L1F_REQUIRE(grid.y <= 65535, L1F_ERR_UNSUPPORTED, "reconstruct: too many row tiles");
   const int64_t nblk = (int64_t)grid.x * grid.y;
   Scratch part(st);
   const bool want = resid_sq && M;
   if (want) L1F_CUDA_TRY(part.alloc(nblk * 2 * sizeof(double)));
-  if (dtype == L1F_F32)
+  double* pp = want ? (double*)part.p : nullptr;
+  const size_t esz = dtype == L1F_F32 ? 4 : 8;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vec = (!M || (al16(M) && (ldm * esz) % 16 == 0)) && (!L || (al16(L) && (ldl * esz) % 16 == 0)) &&
+                   (!S || (al16(S) && (lds * esz) % 16 == 0));
+#define L1F_STREAM(TT, KM)                                                                                       \
+  reconstruct_stream_kernel<TT, KM><<<grid, 256, 0, st>>>(m, n, k, (const TT*)Af, ldaf, (const TT*)Bf, ldbf,   \
+                                                         (const TT*)M, ldm, (TT*)L, ldl, (TT*)S, lds, pp, vec)
+  if (small) {
+    if (dtype == L1F_F32) {
+      if (k <= 4) L1F_STREAM(float, 4); else if (k <= 8) L1F_STREAM(float, 8);
+      else if (k <= 12) L1F_STREAM(float, 12); else L1F_STREAM(float, 16);
+    } else {
+      if (k <= 4) L1F_STREAM(double, 4); else if (k <= 8) L1F_STREAM(double, 8);
+      else if (k <= 12) L1F_STREAM(double, 12); else L1F_STREAM(double, 16);
+    }
+  } else if (dtype == L1F_F32)
     reconstruct_kernel<float><<<grid, kTileThreads, 0, st>>>(
         m, n, k, (const float*)Af, ldaf, (const float*)Bf, ldbf, (const float*)M, ldm, (float*)L, ldl,
-        (float*)S, lds, want ? (double*)part.p : nullptr);
+        (float*)S, lds, pp);
   else
     reconstruct_kernel<double><<<grid, kTileThreads, 0, st>>>(
         m, n, k, (const double*)Af, ldaf, (const double*)Bf, ldbf, (const double*)M, ldm, (double*)L, ldl,
-        (double*)S, lds, want ? (double*)part.p : nullptr);
+        (double*)S, lds, pp);
+#undef L1F_STREAM
   L1F_CHECK_LAUNCH();
   if (want) {
     sum_pairs_kernel<<<1, 1024, 0, st>>>((const double*)part.p, nblk, resid_sq);
