@@ -207,12 +207,12 @@ template <> struct Vec4g<double> {
 };
 
 template <typename T, int KM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 reconstruct_stream_kernel(int64_t m, int64_t n, int k, const T* __restrict__ Af, int64_t ldaf,
                           const T* __restrict__ Bf, int64_t ldbf, const T* __restrict__ M, int64_t ldm,
                           T* __restrict__ L, int64_t ldl, T* __restrict__ S, int64_t lds, double* __restrict__ part,
                           bool vec) {
-  constexpr int TR = 64, TC = 128, RPT = 8;
+  constexpr int TR = 32, TC = 128, RPT = 4;
   __shared__ T as[TR][KM + 1];
   const int tid = threadIdx.x, tc = tid % 32, tr = tid / 32;
   const int64_t r0 = (int64_t)blockIdx.y * TR, c0 = (int64_t)blockIdx.x * TC + 4 * tc;
@@ -521,7 +521,7 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
   if (resid_sq) L1F_CUDA_TRY(cudaMemsetAsync(resid_sq, 0, 2 * sizeof(double), st));
   if (m == 0 || n == 0) return L1F_OK;
   const bool small = k <= 16;
-  dim3 grid = small ? dim3((unsigned)ceil_div(n, 128), (unsigned)ceil_div(m, 64))
+  dim3 grid = small ? dim3((unsigned)ceil_div(n, 128), (unsigned)ceil_div(m, 32))
                     : dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(m, kTile));
   L1F_REQUIRE(grid.y <= 65535, L1F_ERR_UNSUPPORTED, "reconstruct: too many row tiles");
   const int64_t nblk = (int64_t)grid.x * grid.y;
@@ -538,8 +538,16 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
                                                          (const TT*)M, ldm, (TT*)L, ldl, (TT*)S, lds, pp, vec)
   if (small) {
     if (dtype == L1F_F32) {
-      if (k <= 4) L1F_STREAM(float, 4); else if (k <= 8) L1F_STREAM(float, 8);
-      else if (k <= 12) L1F_STREAM(float, 12); else L1F_STREAM(float, 16);
+      switch ((k + 1) / 2) {
+        case 0: case 1: L1F_STREAM(float, 2); break;
+        case 2: L1F_STREAM(float, 4); break;
+        case 3: L1F_STREAM(float, 6); break;
+        case 4: L1F_STREAM(float, 8); break;
+        case 5: L1F_STREAM(float, 10); break;
+        case 6: L1F_STREAM(float, 12); break;
+        case 7: L1F_STREAM(float, 14); break;
+        default: L1F_STREAM(float, 16); break;
+      }
     } else {
       if (k <= 4) L1F_STREAM(double, 4); else if (k <= 8) L1F_STREAM(double, 8);
       else if (k <= 12) L1F_STREAM(double, 12); else L1F_STREAM(double, 16);
