@@ -16,13 +16,25 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// keep freed stream-ordered allocations in the default pool (the default release threshold of
+// 0 returns them to the driver at every synchronisation and re-maps them on the next call)
+static void keep_pool_memory(int dev) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 int num_sms() {
   static int cached = 0;
   if (!cached) {
     int dev = 0, v = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) {
       cached = v;
+      keep_pool_memory(dev);
+    }
     else
       cached = 148;
   }

@@ -494,6 +494,10 @@ static int grid_for(int64_t work, int threads) {
 
 using namespace l1f;
 
+int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t ldaf, const float* Bf, int64_t ldbf,
+                       const float* M, int64_t ldm, float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
+                       cudaStream_t st);
+
 // ====================================================================== C ABI
 extern "C" int l1f_gemm_nt(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
                            int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
@@ -520,6 +524,11 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
   cudaStream_t st = (cudaStream_t)stream;
   if (resid_sq) L1F_CUDA_TRY(cudaMemsetAsync(resid_sq, 0, 2 * sizeof(double), st));
   if (m == 0 || n == 0) return L1F_OK;
+  if (dtype == L1F_F32 && k > 16) {  // tcgen05 3xTF32 path (recon_tc.cu)
+    const int rc = l1f_reconstruct_tc(m, n, k, (const float*)Af, ldaf, (const float*)Bf, ldbf, (const float*)M, ldm,
+                                      (float*)L, ldl, (float*)S, lds, resid_sq, st);
+    if (rc != L1F_ERR_UNSUPPORTED) return rc;
+  }
   const bool small = k <= 16;
   dim3 grid = small ? dim3((unsigned)ceil_div(n, 128), (unsigned)ceil_div(m, 32))
                     : dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(m, kTile));

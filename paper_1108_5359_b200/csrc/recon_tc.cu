@@ -1,0 +1,441 @@
+// Tensor-core reconstruction L = Af Bf^T, S = M - L (K4 for k > 16) on tcgen05.
+//
+// Reference: nystrom_complete + assemble + s = m - l (pkg/src/l1pcp/l1filter.py:137-167,253) in the
+// unified rank-k form L[i][j] = Af[i] . Bf[j] (see l1f_build_factors).  FP32 accuracy from TF32
+// tensor cores by the 3-pass split: x = hi + lo with hi = x with the low 13 mantissa bits cleared
+// (exact in TF32) and lo = x - hi, and L = Ah Bh^T + Ah Bl^T + Al Bh^T accumulated in FP32 in
+// TMEM (error ~2^-22 relative per product; the parity gate is 1e-4).
+//
+// Persistent CTAs (one per SM), 12 warps:
+//   warp 0      TMA producer: fp32 chunks of Af (128 x 32) and Bf (128 x 32), SWIZZLE_128B, K-major
+//   warp 1      TMEM allocation + MMA issuer (one thread): 12 tcgen05.mma.kind::tf32 per chunk
+//   warps 4-7   splitters: hi in place, lo into a second buffer (same swizzled layout)
+//   warps 8-11  epilogue: tcgen05.ld (row per thread), M via TMA (double buffered), S = M - L,
+//               L and S staged in shared memory and written with TMA stores
+// Two 128x128 FP32 accumulators in TMEM (256 columns) overlap the MMA of tile t+1 with the
+// epilogue of tile t; two smem stages overlap loads, splits and MMAs.  Edges are handled by TMA
+// (zero fill on load, clipping on store).  12 B of DRAM traffic per output entry.
+#include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+namespace l1f {
+namespace rtc {
+
+constexpr int BM = 128, BN = 128, BK = 16;      // K chunk of 16 fp32 = 64-byte rows (SWIZZLE_64B)
+constexpr int STAGES = 3;
+constexpr int NMB = 6;                          // M buffers (prefetch distance 4 chunks)
+constexpr int NTHREADS = 384;
+constexpr uint32_t OP_BYTES = BM * BK * 4;      // 8 KB: one 128 x 16 fp32 operand box
+constexpr uint32_t CHUNK_BYTES = BM * 32 * 4;   // 16 KB: one 128 x 32 fp32 epilogue box (SWIZZLE_128B)
+constexpr int GROUP = 8;                        // row tiles per raster group (L2 reuse of Bf)
+
+struct Smem {
+  // every buffer is a multiple of 1024 bytes (swizzle atoms)
+  uint8_t a_raw[STAGES][OP_BYTES];
+  uint8_t b_raw[STAGES][OP_BYTES];
+  uint8_t a_lo[STAGES][OP_BYTES];
+  uint8_t b_lo[STAGES][OP_BYTES];
+  uint8_t mbuf[NMB][CHUNK_BYTES];  // M chunk, overwritten in place by S before its TMA store
+  uint8_t lbuf[2][CHUNK_BYTES];
+  unsigned long long full[STAGES], conv[STAGES], empty[STAGES];
+  unsigned long long tfull[2], tempty[2];
+  unsigned long long mfull[NMB];
+  uint32_t tmem_base;
+  double red[2][4];
+};
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(void* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_arrive(void* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(sa(b)), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int x, int y, void* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(sa(dst)), "l"(map), "r"(x), "r"(y), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(map), "r"(x), "r"(y), "r"(sa(src)) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B (64-byte rows), 8-row groups 512 B apart
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                  // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;         // stride byte offset: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;                  // descriptor version (Blackwell)
+  d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
+  return d;
+}
+// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
+               ::"r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void mma_commit(void* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar))
+               : "memory");
+}
+
+struct Sched {
+  int ntm, ntn, ntiles;
+  __device__ void tile(int t, int& tm, int& tn) const {
+    const int per_group = GROUP * ntn;
+    const int g = t / per_group, r = t - g * per_group;
+    const int gs = min(GROUP, ntm - g * GROUP);
+    tm = g * GROUP + r % gs;
+    tn = r / gs;
+  }
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmL,
+                const __grid_constant__ CUtensorMap tmS, int kchunks, Sched sch, int has_m, int has_l, int has_s,
+                double* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.conv[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 128); }
+    for (int b = 0; b < NMB; ++b) mbar_init(&sm.mfull[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // 256 TMEM columns: two 128-column FP32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < sch.ntiles; t += gridDim.x) {
+        int tm, tn;
+        sch.tile(t, tm, tn);
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const int s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&sm.empty[s], ph ^ 1);
+          mbar_expect_arrive(&sm.full[s], 2 * OP_BYTES);
+          tma_load(sm.a_raw[s], &tmA, kc * BK, tm * BM, &sm.full[s]);
+          tma_load(sm.b_raw[s], &tmB, kc * BK, tn * BN, &sm.full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    int it = 0, ti = 0;
+    for (int t = blockIdx.x; t < sch.ntiles; t += gridDim.x, ++ti) {
+      const int acc = ti & 1, aph = (ti >> 1) & 1;
+      mbar_wait(&sm.tempty[acc], aph ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % STAGES, ph = (it / STAGES) & 1;
+        mbar_wait(&sm.conv[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t ah = sa(sm.a_raw[s]), bh = sa(sm.b_raw[s]), al = sa(sm.a_lo[s]), bl = sa(sm.b_lo[s]);
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t off = 32u * j;  // 8 tf32 = 32 bytes along K inside the 64-byte swizzle atom
+            mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), (kc | j) ? 1u : 0u);
+            mma_tf32(d, smem_desc(ah + off), smem_desc(bl + off), 1u);
+            mma_tf32(d, smem_desc(al + off), smem_desc(bh + off), 1u);
+          }
+          mma_commit(&sm.empty[s]);                         // stage free when these MMAs retire
+          if (kc == kchunks - 1) mma_commit(&sm.tfull[acc]);  // accumulator ready
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ================= hi / lo split (128 threads)
+    const int ct = threadIdx.x - 128;
+    int it = 0;
+    for (int t = blockIdx.x; t < sch.ntiles; t += gridDim.x) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const int s = it % STAGES, ph = (it / STAGES) & 1;
+        mbar_wait(&sm.full[s], ph);
+        uint4* ar = reinterpret_cast<uint4*>(sm.a_raw[s]);
+        uint4* br = reinterpret_cast<uint4*>(sm.b_raw[s]);
+        float4* alo = reinterpret_cast<float4*>(sm.a_lo[s]);
+        float4* blo = reinterpret_cast<float4*>(sm.b_lo[s]);
+#pragma unroll 4
+        for (int e = ct; e < (int)(OP_BYTES / 16); e += 128) {
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            uint4* raw = w ? br : ar;
+            float4* lo = w ? blo : alo;
+            uint4 x = raw[e];
+            uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
+            lo[e] = make_float4(__uint_as_float(x.x) - __uint_as_float(h.x), __uint_as_float(x.y) - __uint_as_float(h.y),
+                                __uint_as_float(x.z) - __uint_as_float(h.z), __uint_as_float(x.w) - __uint_as_float(h.w));
+            raw[e] = h;
+          }
+        }
+        fence_async_smem();
+        named_bar(2, 128);
+        if (ct == 0) mbar_arrive(&sm.conv[s]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ================= epilogue (128 threads, TMEM lane quarter = warp - 8)
+    const int q = warp - 8, row = 32 * q + lane;  // row of the tile owned by this thread
+    const bool leader = threadIdx.x == 256;
+    double r2 = 0.0, m2 = 0.0;
+    int ti = 0, g = 0;
+    // chunk g -> (tile, column chunk); prefetch M of chunk g+1 while g is processed
+    auto chunk_coords = [&](int gg, int& x, int& y) -> bool {
+      const int tloc = gg / (BN / 32), cc = gg % (BN / 32);
+      const int t = blockIdx.x + tloc * gridDim.x;
+      if (t >= sch.ntiles) return false;
+      int tm, tn;
+      sch.tile(t, tm, tn);
+      x = tn * BN + cc * 32;
+      y = tm * BM;
+      return true;
+    };
+    if (leader && has_m) {  // M of the first four chunks
+      for (int gg = 0; gg < 4; ++gg) {
+        int x, y;
+        if (chunk_coords(gg, x, y)) {
+          mbar_expect_arrive(&sm.mfull[gg], CHUNK_BYTES);
+          tma_load(sm.mbuf[gg], &tmM, x, y, &sm.mfull[gg]);
+        }
+      }
+    }
+    for (int t = blockIdx.x; t < sch.ntiles; t += gridDim.x, ++ti) {
+      int tm, tn;
+      sch.tile(t, tm, tn);
+      const int acc = ti & 1, aph = (ti >> 1) & 1;
+      mbar_wait(&sm.tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int cc = 0; cc < BN / 32; ++cc, ++g) {
+        const int mb = g % NMB, lb = g & 1;
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t)(acc * BN + cc * 32) + ((uint32_t)(32 * q) << 16);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (cc == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(&sm.tempty[acc]);
+        }
+        if (leader) {
+          // stores of chunk g-2 (lbuf[lb], mbuf[(g-2) % NMB]) have finished reading shared memory
+          tma_wait_read1();
+          if (has_m) {  // prefetch M of chunk g+4 into the buffer freed above
+            int x, y;
+            if (chunk_coords(g + 4, x, y)) {
+              const int nb = (g + 4) % NMB;
+              mbar_expect_arrive(&sm.mfull[nb], CHUNK_BYTES);
+              tma_load(sm.mbuf[nb], &tmM, x, y, &sm.mfull[nb]);
+            }
+          }
+        }
+        if (has_m) mbar_wait(&sm.mfull[mb], (g / NMB) & 1);
+        named_bar(1, 128);
+        // 16-byte chunk j of this row sits at position j ^ (row & 7) (SWIZZLE_128B)
+        float4* mrow = reinterpret_cast<float4*>(sm.mbuf[mb] + row * 128);
+        float4* lrow = reinterpret_cast<float4*>(sm.lbuf[lb] + row * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int p = j ^ (row & 7);
+          const float4 l4 = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                        __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          if (has_l) lrow[p] = l4;
+          if (has_m) {
+            const float4 m4 = mrow[p];
+            const float4 s4 = make_float4(m4.x - l4.x, m4.y - l4.y, m4.z - l4.z, m4.w - l4.w);
+            mrow[p] = s4;  // S in place of M (each thread owns its row)
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w},
+                        ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double dd = (double)((mm[u] - ll[u]) - ss[u]);
+              r2 += dd * dd;
+              m2 += (double)mm[u] * (double)mm[u];
+            }
+          }
+        }
+        fence_async_smem();
+        named_bar(1, 128);
+        if (leader) {
+          const int x = tn * BN + cc * 32, y = tm * BM;
+          if (has_l) tma_store(&tmL, x, y, sm.lbuf[lb]);
+          if (has_s && has_m) tma_store(&tmS, x, y, sm.mbuf[mb]);
+          tma_commit();
+        }
+      }
+    }
+    if (leader) tma_wait_all();
+    // per-CTA residual partials (deterministic)
+    r2 = warp_sum(r2);
+    m2 = warp_sum(m2);
+    if (lane == 0) { sm.red[0][q] = r2; sm.red[1][q] = m2; }
+    named_bar(1, 128);
+    if (leader && part) {
+      double a = 0, c = 0;
+      for (int i = 0; i < 4; ++i) { a += sm.red[0][i]; c += sm.red[1][i]; }
+      part[2 * blockIdx.x] = a;
+      part[2 * blockIdx.x + 1] = c;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// zero-padded copy of a rows x k factor to rows x kp (TMA needs a 16-byte row pitch; kp % 16 == 0)
+__global__ void pad_factor_kernel(const float* __restrict__ src, int64_t rows, int k, int64_t lds, int kp,
+                                  float* __restrict__ dst) {
+  const int64_t total = rows * (int64_t)kp;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / kp;
+    const int t = (int)(e - r * kp);
+    dst[e] = t < k ? src[r * lds + t] : 0.0f;
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int i = 0; i < n; ++i) { a += part[2 * i]; b += part[2 * i + 1]; }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D fp32 tensor (rows x cols, row pitch ld elements), box_cols x 128 boxes
+static bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                     CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace rtc
+}  // namespace l1f
+
+// tcgen05 path of l1f_reconstruct for float, k > 16; returns L1F_ERR_UNSUPPORTED when it cannot run
+int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t ldaf, const float* Bf, int64_t ldbf,
+                       const float* M, int64_t ldm, float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
+                       cudaStream_t st) {
+  using namespace l1f;
+  using namespace l1f::rtc;
+  const char* env = getenv("L1F_RECON_TC");
+  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  if ((M && (!al16(M) || ldm % 4)) || (L && (!al16(L) || ldl % 4)) || (S && (!al16(S) || lds % 4)))
+    return L1F_ERR_UNSUPPORTED;
+  if (m >= INT32_MAX || n >= INT32_MAX || !encode_fn()) return L1F_ERR_UNSUPPORTED;
+  const int kp = (int)ceil_div(k, BK) * BK;
+  float *ap = nullptr, *bp = nullptr;
+  double* part = nullptr;
+  const int grid = num_sms();
+  L1F_CUDA_TRY(cudaMallocAsync(&ap, sizeof(float) * (size_t)m * kp, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&bp, sizeof(float) * (size_t)n * kp, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * 2 * grid, st));
+  pad_factor_kernel<<<grid * 4, 256, 0, st>>>(Af, m, k, ldaf, kp, ap);
+  pad_factor_kernel<<<grid * 4, 256, 0, st>>>(Bf, n, k, ldbf, kp, bp);
+  CUtensorMap tA, tB, tM, tL, tS;
+  const auto W = CU_TENSOR_MAP_SWIZZLE_128B;
+  bool ok = make_map(&tA, ap, m, kp, kp, BK, CU_TENSOR_MAP_SWIZZLE_64B) &&
+            make_map(&tB, bp, n, kp, kp, BK, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok = ok && make_map(&tM, M ? (const void*)M : (const void*)ap, M ? m : 1, M ? n : 32, M ? ldm : 32, 32, W);
+  ok = ok && make_map(&tL, L ? (const void*)L : (const void*)ap, L ? m : 1, L ? n : 32, L ? ldl : 32, 32, W);
+  ok = ok && make_map(&tS, S ? (const void*)S : (const void*)ap, S ? m : 1, S ? n : 32, S ? lds : 32, 32, W);
+  int rc = L1F_OK;
+  if (!ok) {
+    set_error("reconstruct: cuTensorMapEncodeTiled failed");
+    rc = L1F_ERR_UNSUPPORTED;
+  } else {
+    Sched sch;
+    sch.ntm = (int)ceil_div(m, BM);
+    sch.ntn = (int)ceil_div(n, BN);
+    sch.ntiles = sch.ntm * sch.ntn;
+    const size_t smem = sizeof(Smem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int g = std::min(grid, sch.ntiles);
+    // L1F_RECON_TC_MASK (diagnostics): bit 0 drops M, bit 1 drops L, bit 2 drops S
+    const char* mk = getenv("L1F_RECON_TC_MASK");
+    const int mask = mk ? atoi(mk) : 0;
+    recon_tc_kernel<<<g, NTHREADS, smem, st>>>(tA, tB, tM, tL, tS, kp / BK, sch, M != nullptr && !(mask & 1),
+                                               L != nullptr && !(mask & 2), S != nullptr && !(mask & 4), part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error("reconstruct (tcgen05): launch failed: %s", cudaGetErrorString(e));
+      rc = L1F_ERR_CUDA;
+    } else if (resid_sq && M) {
+      sum_parts_kernel<<<1, 32, 0, st>>>(part, g, resid_sq);
+    }
+  }
+  cudaFreeAsync(ap, st);
+  cudaFreeAsync(bp, st);
+  cudaFreeAsync(part, st);
+  return rc;
+}
