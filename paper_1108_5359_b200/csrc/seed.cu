@@ -15,6 +15,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace l1f {
@@ -220,6 +221,112 @@ static int svt_into(Handles* h, const double* W, int64_t m, int64_t n, double et
   return L1F_OK;
 }
 
+// SVT through the eigendecomposition of the smaller Gram matrix (used inside the ALM loop):
+// W^T W = V diag(sigma^2) V^T (or W W^T = U diag(sigma^2) U^T when m < n), then
+// out = W V_k diag(1 - eta/sigma_k) V_k^T.  Squaring the spectrum costs relative accuracy only in
+// singular values far below sigma_max, whose SVT contribution (sigma - eta) is absolutely tiny, so
+// the thresholded matrix matches the SVD form to ~eps * sigma_max per entry; the seed's final
+// rank-revealing factorisation still uses the SVD (svd_rowmajor).
+__global__ void scale_rows_cm_kernel(double* __restrict__ T, int64_t rows, int64_t cols, int64_t ld,
+                                     const double* __restrict__ c) {
+  // column-major T (rows x cols): row j scaled by c[j]
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = e / rows, j = e - col * rows;
+    T[col * ld + j] *= c[j];
+  }
+}
+__global__ void scale_cols_cm_kernel(double* __restrict__ T, int64_t rows, int64_t cols, int64_t ld,
+                                     const double* __restrict__ c) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = e / rows, i = e - col * rows;
+    T[col * ld + i] *= c[col];
+  }
+}
+
+static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
+                    cudaStream_t st) {
+  const bool right = n <= m;         // Gram of the smaller side
+  const int p = (int)(right ? n : m), q = (int)(right ? m : n);
+  // row-major W (m x n) == column-major X = W^T (n x m, ld n)
+  Buf g(st), ev(st), work(st), info(st), t(st), cbuf(st);
+  L1F_CUDA_TRY(g.alloc(sizeof(double) * (size_t)p * p));
+  L1F_CUDA_TRY(ev.alloc(sizeof(double) * (size_t)p));
+  const double one = 1.0, zero = 0.0;
+  cublasSetPointerMode(h->blas, CUBLAS_POINTER_MODE_HOST);
+  if (right)  // W^T W = X X^T
+    cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)n, &zero, g.d(), p);
+  else        // W W^T = X^T X
+    cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)n, &zero, g.d(), p);
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
+                                  &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("syevd_bufferSize failed");
+    return L1F_ERR_CUDA;
+  }
+  L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
+  L1F_CUDA_TRY(info.alloc(sizeof(int)));
+  if (cusolverDnDsyevd(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
+                       (int*)info.p) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("cusolverDnDsyevd failed");
+    return L1F_ERR_SVD;
+  }
+  std::vector<double> lam((size_t)p);
+  int info_h = 0;
+  L1F_CUDA_TRY(cudaMemcpyAsync(lam.data(), ev.p, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaMemcpyAsync(&info_h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  if (info_h != 0) {
+    set_error("eigendecomposition failed on (%lld, %lld) matrix: syevd info %d", (long long)m, (long long)n, info_h);
+    return L1F_ERR_SVD;
+  }
+  // eigenvalues ascending: the k largest with sigma > eta occupy the last k columns
+  int k = 0;
+  std::vector<double> c;
+  for (int j = p - 1; j >= 0; --j) {
+    const double sg = lam[(size_t)j] > 0.0 ? std::sqrt(lam[(size_t)j]) : 0.0;
+    if (!(sg > 0.0) || !(sg - eta > 0.0)) break;
+    ++k;
+  }
+  *rank = k;
+  if (k == 0) {
+    L1F_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)m * n, st));
+    return L1F_OK;
+  }
+  c.resize((size_t)k);
+  for (int i = 0; i < k; ++i) {  // columns p-k .. p-1 in ascending order
+    const double sg = std::sqrt(lam[(size_t)(p - k + i)]);
+    c[(size_t)i] = 1.0 - eta / sg;
+  }
+  L1F_CUDA_TRY(cbuf.alloc(sizeof(double) * (size_t)k));
+  L1F_CUDA_TRY(cudaMemcpyAsync(cbuf.p, c.data(), sizeof(double) * (size_t)k, cudaMemcpyHostToDevice, st));
+  const double* Vk = g.d() + (size_t)(p - k) * p;  // column-major p x k block of eigenvectors
+  L1F_CUDA_TRY(t.alloc(sizeof(double) * (size_t)k * q));
+  if (right) {
+    // Tt (k x m) = Vk^T X ; scale row j by c_j ; out^T (n x m) = Vk Tt
+    cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)m, (int)n, &one, Vk, p, W, (int)n, &zero, t.d(), k);
+    scale_rows_cm_kernel<<<num_sms() * 4, 256, 0, st>>>(t.d(), k, m, k, cbuf.d());
+    cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, k, &one, Vk, p, t.d(), k, &zero, out, (int)n);
+  } else {
+    // T (n x k) = X Uk ; scale column j by c_j ; out^T (n x m) = T Uk^T
+    cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, k, (int)m, &one, W, (int)n, Vk, p, &zero, t.d(), (int)n);
+    scale_cols_cm_kernel<<<num_sms() * 4, 256, 0, st>>>(t.d(), n, k, n, cbuf.d());
+    cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)m, k, &one, t.d(), (int)n, Vk, p, &zero, out, (int)n);
+  }
+  L1F_CHECK_LAUNCH();
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));  // keep the host vector alive until consumed
+  return L1F_OK;
+}
+
+// ALM-loop SVT: Gram/eigen form for seed-sized and larger matrices (L1F_SEED_SVT=gesvd forces the SVD)
+static int svt_loop(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
+                    cudaStream_t st) {
+  const char* mode = getenv("L1F_SEED_SVT");
+  const bool use_svd = (mode && mode[0] == 'g') || (m < 128 && n < 128);
+  return use_svd ? svt_into(h, W, m, n, eta, out, rank, st) : svt_gram(h, W, m, n, eta, out, rank, st);
+}
+
 static int spectral_norm(Handles* h, const double* M, int64_t m, int64_t n, int iters, double* out, cudaStream_t st) {
   // row-major M (m x n) == column-major A = M^T (n x m, ld n)
   Buf v(st), w(st);
@@ -333,7 +440,7 @@ extern "C" int l1f_pcp_f64(const double* M, int64_t m, int64_t n, double lam, do
   for (it = 1; it <= max_iter; ++it) {
     pcp_shrink_kernel<<<eg, 256, 0, st>>>(M, L, y.d(), S, w.d(), count, beta, lam / beta);
     L1F_CHECK_LAUNCH();
-    rc = svt_into(h, w.d(), m, n, 1.0 / beta, L, &rank, st);
+    rc = svt_loop(h, w.d(), m, n, 1.0 / beta, L, &rank, st);
     if (rc) return rc;
     pcp_residual_kernel<<<g, 256, 0, st>>>(M, L, S, y.d(), count, beta, part.d());
     L1F_CHECK_LAUNCH();
