@@ -437,10 +437,29 @@ int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T*
                        int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
                        bool query, size_t* need);
 
+int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
+                    double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
+                    float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
+                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+
 namespace l1f {
 namespace filt {
 
-// small-k group kernel (filter_small.cu), resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
+template <typename T>
+int tc_dispatch(const T*, int64_t, int, int64_t, const T*, int64_t, int, double, double, double, double, int, T*,
+                int64_t, T*, int64_t, int32_t*, T*, uint8_t*, void*, size_t, cudaStream_t, bool, size_t*) {
+  return L1F_ERR_UNSUPPORTED;  // fp64: no tensor-core path
+}
+template <>
+int tc_dispatch<float>(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
+                       double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
+                       float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
+                       size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+  return l1f_tc_dispatch(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, iters,
+                         res, status, workspace, ws_bytes, st, query, need);
+}
+
+// small-k group kernel (filter_small.cu), tensor-core kernel (filter_tc.cu, fp32), resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
 template <typename T>
 int select(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
            double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
@@ -450,6 +469,9 @@ int select(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
     const int rs = l1f_small_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz,
                                          E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
     if (rs != L1F_ERR_UNSUPPORTED) return rs;
+    const int rt = tc_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde,
+                                  iters, res, status, workspace, ws_bytes, st, query, need);
+    if (rt != L1F_ERR_UNSUPPORTED) return rt;
     const int rc = l1f_resident_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z,
                                             ldz, E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
     if (rc != L1F_ERR_UNSUPPORTED) return rc;
