@@ -2,23 +2,29 @@
 // contractions of every ADM iteration on tcgen05.
 //
 // Reference: _solve_block, pkg/src/l1pcp/l1reg.py:59-137 (per-unit ADM for min ||x - A z||_1).
-// Per pass (one ADM iteration of the 32 unit slots of a cluster) a CTA owning SL = 128 dictionary
-// rows computes
-//   phase a   az[row][slot]  = sum_t A[row][t] z[t][slot]     tcgen05.mma M=128 (rows) N=32 K=k
+// A cluster of C = ceil(s / 128) CTAs keeps the s x k dictionary resident (CTA c: rows
+// [128 c, 128 c + 128)).  Each CTA runs TWO independent slot groups of 32 units (warps 0-7 and
+// 8-15); a group's pass is one ADM iteration of its 32 units:
+//   phase a   az[row][slot] = sum_t A[row][t] z[t][slot]      tcgen05.mma M=128 (rows) N=32 K=k
 //   phase b   the elementwise ADM update of filter_resident.cu (cancellation-free residual)
-//   phase c   zp[t][slot]    = sum_row A[row][t] v[row][slot]  tcgen05.mma M=128 (t)    N=32 K=128
-// and the cluster sums zp over its CTAs through DSMEM as in filter_resident.cu.
+//   phase c   zp[t][slot]   = sum_row A[row][t] v[row][slot]   tcgen05.mma M=128 (t)    N=32 K=128
+//   exchange  round 1: each thread pushes its TMEM rows of zp straight to the CTA owning them
+//             (DSMEM st.async) with the per-slot max|r|; the per-unit decision follows; round 2:
+//             owners sum their slice, split it into the bf16 pieces of the phase-a operand and
+//             push those to every CTA.
+// The two groups share the dictionary and the tensor core; one group's MMAs overlap the other
+// group's elementwise work and DSMEM latency.
 //
 // FP32 accuracy from BF16 tensor cores: every operand is split into three bf16 pieces
 // x = x0 + x1 + x2 (each the bf16 rounding of the remainder; 24 significant bits) and the
 // products with i + j <= 2 are accumulated in FP32 in TMEM (6 MMAs per K step; the dropped terms
 // are ~2^-26 relative).  bf16 because tcgen05 reads bf16 operands in MN-major layout (TF32 only
-// K-major): the dictionary's no-swizzle core matrices (8 rows x 8 columns, 16-byte rows) are
-// K-major for phase a (M = rows) and MN-major for phase c (M = columns), so ONE resident copy of A
-// (3 pieces, 6 B per element) serves both contractions.
+// K-major, tools/umma_debug.cu): the dictionary's no-swizzle core matrices (8 rows x 8 columns,
+// 16-byte rows) are K-major for phase a (M = rows) and MN-major for phase c (M = columns), so ONE
+// resident copy of A (3 pieces, 6 B per element) serves both contractions.
 //
-// Roles: warp 1 (one thread) issues the MMAs; warp 0 takes the per-slot decisions while phase a runs;
-// all 16 warps do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows, slots 8 (w / 4) .. +7).
+// Roles in a group (8 warps): warp 1 lane 0 issues the MMAs, warp 0 takes the per-slot decisions,
+// all 8 warps do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows, slots 16 (w / 4) .. +15).
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -35,14 +41,16 @@ namespace cg = cooperative_groups;
 namespace l1f {
 namespace tcf {
 
-constexpr int TS = 32;        // unit slots per cluster (MMA N)
+constexpr int TS = 32;        // unit slots per group (MMA N)
 constexpr int SL = 128;       // dictionary rows per CTA (MMA M of phase a)
-constexpr int NT = 512;       // threads per CTA (4 warps per TMEM lane quarter)
-constexpr int TSP = TS + 4;   // padded fp32 z row (conflict-free TMEM -> smem stores)
+constexpr int NG = 2;         // slot groups per CTA
+constexpr int GT = 256;       // threads per group
+constexpr int NT = NG * GT;   // threads per CTA
+constexpr int TSP = TS;       // fp32 rows of the partial-z inbox
 constexpr int RING = 4;
 constexpr int kStallIters = 20;      // STAGNATION_ITERS, l1reg.py:34
 constexpr float kStallEps = 1e-12f;  // STAGNATION_EPS, l1reg.py:33
-constexpr uint32_t TMEM_COLS = 64;   // phase a: cols [0, 32); phase c: cols [32, 64)
+constexpr uint32_t TMEM_COLS = 128;  // group g: phase a cols [64 g, 64 g + 32), phase c [64 g + 32, 64 g + 64)
 
 struct Params {
   int s, k, cluster, rs;
@@ -51,38 +59,43 @@ struct Params {
   double tol, rho, beta0, beta_max;
 };
 
-struct Slots {
-  int unit[TS], it[TS], stalled[TS], state[TS], finish[TS], src[TS];
-  float beta_cur[TS], beta_next[TS], inv_next[TS], beta_max[TS], thresh[TS], prev_res[TS], res[TS];
+// dynamic shared memory: dictionary pieces, then one region per group (byte offsets)
+struct Layout {
+  uint32_t group0, gstride;                             // group g region at group0 + g * gstride
+  uint32_t zop, vop, zin, zsl, ring, rall, rpart;       // offsets inside a group region
+  uint32_t total;
+};
+
+struct Group {
+  int unit[TS], it[TS], stalled[TS], state[TS], src[TS];
+  float beta_cur[TS], beta_next[TS], inv_next[TS], beta_max[TS], thresh[TS], prev_res[TS];
+  alignas(16) float4 prm[TS];  // phase-b parameters per slot: beta_it, 1/beta_{it+1}, zero-az flag
   float ring_sc[RING];
   long long ring_u[RING];
   long long head, tail, pf_from, pf_to;
-  alignas(16) float4 prm[TS];  // phase-b parameters per slot: beta_it, 1/beta_{it+1}, zero-az flag
   alignas(8) unsigned long long bar_p, bar_r, bar_a, bar_c;
-  uint32_t tmem, fmask;
-  uint8_t code[TS];
+  uint32_t fmask;
 };
 
 template <int KP>
-struct Geo {
-  static constexpr int KG = KP / 8;                         // 8-column groups of A
-  static constexpr int KZ = KP + 16;                        // fp32 z rows (room for C * ceil(KP / C))
-  static constexpr size_t a_piece = (size_t)SL * KP;       // bf16 elements per piece
-  static constexpr size_t z_piece = (size_t)KP * TS;
-  static constexpr size_t v_piece = (size_t)SL * TS;
-  // bf16 operands first (their MMA over-reads past the last piece land in bf16 data), then fp32
-  static constexpr size_t off_a = 0;
-  static constexpr size_t off_z = off_a + 3 * a_piece * 2;
-  static constexpr size_t off_v = off_z + 3 * z_piece * 2;
-  static constexpr size_t off_z0 = off_v + 3 * v_piece * 2;       // fp32 z ping
-  static constexpr size_t off_z1 = off_z0 + (size_t)KZ * TSP * 4;  // fp32 z pong
-  static constexpr size_t off_zin = off_z1 + (size_t)KZ * TSP * 4; // peers' partials of my slice
-  static constexpr size_t off_rpart = off_zin + (size_t)KZ * TSP * 4;
-  static constexpr size_t off_ring = off_rpart + (size_t)4 * TS * 4;
-  static constexpr size_t off_rall = off_ring + (size_t)RING * SL * 4;
-  static constexpr size_t smem_bytes = off_rall + (size_t)16 * TS * 4;
-  static_assert(KP % 16 == 0 && KP <= 128, "KP: multiple of 16, at most 128 (one phase-c M tile)");
-};
+constexpr uint32_t a_bytes() { return 3u * SL * KP * 2u; }
+
+template <int KP>
+Layout make_layout(int C, int rs) {
+  Layout L;
+  uint32_t o = 0;
+  L.zop = o; o += 3u * KP * TS * 2u;
+  L.vop = o; o += 3u * SL * TS * 2u;
+  L.zin = o; o += (uint32_t)(C * rs) * TSP * 4u;
+  L.zsl = o; o += 2u * (uint32_t)rs * TS * 4u;
+  L.ring = o; o += RING * SL * 4u;
+  L.rall = o; o += 2u * (uint32_t)C * TS * 4u;
+  L.rpart = o; o += 4u * TS * 4u;
+  L.gstride = (o + 127u) & ~127u;
+  L.group0 = a_bytes<KP>();  // bf16 zop of group 0 follows A: phase-c over-reads stay in bf16 data
+  L.total = L.group0 + NG * L.gstride;
+  return L;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t rank) {
@@ -115,6 +128,18 @@ __device__ __forceinline__ void cp_async4(void* dst, const float* src, bool vali
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void st_async16v(uint32_t peer_dst, float a, float b, float c, float d, uint32_t peer_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(peer_dst), "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
+               "r"(__float_as_uint(d)), "r"(peer_bar) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ bool bar_or(int id, int n, bool pred) {
+  uint32_t out;
+  asm volatile("{ .reg .pred p, q; setp.ne.u32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.u32 %0, 1, 0, q; }"
+               : "=r"(out) : "r"((uint32_t)pred), "r"(id), "r"(n) : "memory");
+  return out != 0;
+}
 
 __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -160,21 +185,14 @@ __host__ __device__ constexpr int term_b(int t) { return t == 1 || t == 4 ? 1 : 
 template <int KP>
 __global__ void __launch_bounds__(NT, 1)
 adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t lda, const float* __restrict__ scale,
-              Params P, float* __restrict__ Z, float* __restrict__ E, int32_t* __restrict__ iters,
+              Params P, Layout Lo, float* __restrict__ Z, float* __restrict__ E, int32_t* __restrict__ iters,
               float* __restrict__ res_out, uint8_t* __restrict__ status, long long* __restrict__ prof) {
-  using Gm = Geo<KP>;
-  constexpr int KG = Gm::KG;
+  constexpr int KG = KP / 8;
+  constexpr size_t A_PIECE = (size_t)SL * KP, Z_PIECE = (size_t)KP * TS, V_PIECE = (size_t)SL * TS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __nv_bfloat16* aop = reinterpret_cast<__nv_bfloat16*>(smem_raw + Gm::off_a);  // [3][SL*KP]
-  __nv_bfloat16* zop = reinterpret_cast<__nv_bfloat16*>(smem_raw + Gm::off_z);  // [3][KP*TS]
-  __nv_bfloat16* vop = reinterpret_cast<__nv_bfloat16*>(smem_raw + Gm::off_v);  // [3][SL*TS]
-  float* zbuf0 = reinterpret_cast<float*>(smem_raw + Gm::off_z0);               // [KZ][TSP]
-  float* zbuf1 = reinterpret_cast<float*>(smem_raw + Gm::off_z1);
-  float* zin = reinterpret_cast<float*>(smem_raw + Gm::off_zin);
-  float* rpart = reinterpret_cast<float*>(smem_raw + Gm::off_rpart);            // [4][TS]
-  float* ring_x = reinterpret_cast<float*>(smem_raw + Gm::off_ring);            // [RING][SL]
-  float* rall = reinterpret_cast<float*>(smem_raw + Gm::off_rall);              // [16][TS]
-  __shared__ Slots ss;
+  __shared__ Group groups[NG];
+  __shared__ uint32_t tmem_base;
+  __nv_bfloat16* aop = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [3][SL*KP]
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = P.cluster;
@@ -183,7 +201,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row_base = crank * SL;
   const float tol = (float)P.tol, rho = (float)P.rho;
-  const int rs = P.rs;  // rows of z reduced by each CTA
+  const int rs = P.rs;                              // z rows owned (summed) by each CTA
+  const int r0 = crank * rs;
+  const int vmine = max(0, min(rs, KP - r0));       // valid rows of my slice
 
   // ---- resident dictionary rows, 3 bf16 pieces: core matrix (row group rg, column group cg) at
   //      (rg * KG + cg) * 64 elements, element (r % 8) * 8 + (t % 8)
@@ -195,80 +215,112 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     split3(a, p0, p1, p2);
     const size_t off = (size_t)((r >> 3) * KG + (t >> 3)) * 64 + (r & 7) * 8 + (t & 7);
     aop[off] = p0;
-    aop[Gm::a_piece + off] = p1;
-    aop[2 * Gm::a_piece + off] = p2;
+    aop[A_PIECE + off] = p1;
+    aop[2 * A_PIECE + off] = p2;
   }
-  for (int e = tid; e < (int)(3 * Gm::z_piece); e += NT) zop[e] = __float2bfloat16_rn(0.f);
+  for (int g = 0; g < NG; ++g) {
+    __nv_bfloat16* zo = reinterpret_cast<__nv_bfloat16*>(smem_raw + Lo.group0 + g * Lo.gstride + Lo.zop);
+    for (int e = tid; e < (int)(3 * Z_PIECE); e += NT) zo[e] = __float2bfloat16_rn(0.f);
+  }
+  if (tid == 0) {
+    for (int g = 0; g < NG; ++g) {
+      mbar_init(&groups[g].bar_p, 1);
+      mbar_init(&groups[g].bar_r, 1);
+      mbar_init(&groups[g].bar_a, 1);
+      mbar_init(&groups[g].bar_c, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) umma::tmem_alloc(&tmem_base, TMEM_COLS);
+  umma::fence_async_smem();  // dictionary and zero z operands visible to the tensor core
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  if (C > 1) cluster.sync();  // peers' mbarriers initialised before any DSMEM traffic
 
-  // phase b mapping: TMEM lane quarter q (rows 32q .. 32q+31), slots [8 h, 8 h + 8)
-  const int q = warp & 3, h = warp >> 2;
+  // ================================================================ one slot group
+  const int g = warp / 8, gw = warp % 8, gtid = tid % GT;
+  const int gbar = 1 + g, sbar = 3 + g;  // named barriers: whole group / warps 1-7 of the group
+  Group& G = groups[g];
+  unsigned char* gb = smem_raw + Lo.group0 + g * Lo.gstride;
+  __nv_bfloat16* zop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.zop);  // [3][KP*TS] phase-a operand
+  __nv_bfloat16* vop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.vop);  // [3][SL*TS] phase-c operand
+  float* zin = reinterpret_cast<float*>(gb + Lo.zin);      // [C*rs][TSP] partials of my slice, by sender
+  float* zsl = reinterpret_cast<float*>(gb + Lo.zsl);      // [2][rs][TS] reduced slice (pass parity)
+  float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RING][SL]
+  float* rall = reinterpret_cast<float*>(gb + Lo.rall);    // [2][C][TS] per-CTA slot max|r| (parity)
+  float* rpart = reinterpret_cast<float*>(gb + Lo.rpart);  // [4][TS]
+  const uint32_t tmem = tmem_base + 64u * g;
+  const int vid = cid * NG + g, nv = nclusters * NG;      // units vid, vid + nv, ...
+
+  // phase b mapping: TMEM lane quarter q (rows 32q .. 32q+31), slots [16 h, 16 h + 16)
+  const int q = gw & 3, h = gw >> 2;
   const int lrow = 32 * q + lane;
   const int grow = row_base + lrow;
-  const int slot0 = 8 * h;
+  const int slot0 = 16 * h;
+  float xr[16], yr[16], lr[16];
 
-  float xr[8], yr[8], lr[8];
-
-  auto cand = [&](long long j) -> long long { return (long long)cid + j * (long long)nclusters; };
+  auto cand = [&](long long j) -> long long { return (long long)vid + j * (long long)nv; };
   auto prefetch = [&]() {
-    for (long long j = ss.pf_from; j < ss.pf_to; ++j) {
+    for (long long j = G.pf_from; j < G.pf_to; ++j) {
       const int e = (int)(j % RING);
       const long long u = cand(j);
       const bool ok = u < P.n_units;
-      for (int r = tid; r < SL; r += NT)
+      for (int r = gtid; r < SL; r += GT)
         cp_async4(ring_x + (size_t)e * SL + r, X + (ok ? u : 0) * P.ldx + (ok && row_base + r < P.s ? row_base + r : 0),
                   ok && row_base + r < P.s);
-      if (tid == 0) {
-        ss.ring_u[e] = u;
-        cp_async4(&ss.ring_sc[e], scale + (ok ? u : 0), ok);
+      if (gtid == 0) {
+        G.ring_u[e] = u;
+        cp_async4(&G.ring_sc[e], scale + (ok ? u : 0), ok);
       }
     }
   };
   auto install_unit = [&](int slot, long long u, float sc, int src) {
     const float b0 = P.beta0 > 0 ? (float)P.beta0 : 1.f / sc;
-    ss.unit[slot] = (int)u;
-    ss.state[slot] = 1;
-    ss.it[slot] = 0;
-    ss.stalled[slot] = 0;
-    ss.src[slot] = src;
-    ss.beta_cur[slot] = b0;
-    ss.beta_next[slot] = b0;
-    ss.inv_next[slot] = 1.f / b0;
-    ss.beta_max[slot] = P.beta_max > 0 ? (float)P.beta_max : 1e7f * b0;
-    ss.thresh[slot] = tol * sc;
-    ss.prev_res[slot] = Limits<float>::inf();
+    G.unit[slot] = (int)u;
+    G.state[slot] = 1;
+    G.it[slot] = 0;
+    G.stalled[slot] = 0;
+    G.src[slot] = src;
+    G.beta_cur[slot] = b0;
+    G.beta_next[slot] = b0;
+    G.inv_next[slot] = 1.f / b0;
+    G.beta_max[slot] = P.beta_max > 0 ? (float)P.beta_max : 1e7f * b0;
+    G.thresh[slot] = tol * sc;
+    G.prev_res[slot] = Limits<float>::inf();
   };
   auto claim_into = [&](int slot) {
     for (;;) {
-      if (ss.head < ss.tail) {
-        const int e = (int)(ss.head % RING);
-        const long long u = ss.ring_u[e];
-        ss.head++;
+      if (G.head < G.tail) {
+        const int e = (int)(G.head % RING);
+        const long long u = G.ring_u[e];
+        G.head++;
         if (u >= P.n_units) break;
-        if (ss.ring_sc[e] > 0.f) { install_unit(slot, u, ss.ring_sc[e], e); return; }
+        if (G.ring_sc[e] > 0.f) { install_unit(slot, u, G.ring_sc[e], e); return; }
       } else {
-        const long long u = cand(ss.head);
-        ss.head++;
-        ss.tail = ss.head;
+        const long long u = cand(G.head);
+        G.head++;
+        G.tail = G.head;
         if (u >= P.n_units) break;
         const float sc = scale[u];
         if (sc > 0.f) { install_unit(slot, u, sc, -1); return; }
       }
     }
-    ss.state[slot] = 0;
-    ss.unit[slot] = -1;
+    G.state[slot] = 0;
+    G.unit[slot] = -1;
   };
-  // warp 0, lane = slot: phase-b parameters of this pass (after the decision and the claims)
+  // warp 0 of the group, lane = slot: phase-b parameters of the next pass
   auto publish = [&](int slot) {
-    const bool live = ss.state[slot] == 1;
-    const bool zero_az = !live || ss.it[slot] == 0;  // fresh or empty slot: A z_0 = 0
-    ss.prm[slot] = live ? make_float4(ss.beta_cur[slot], ss.inv_next[slot], zero_az ? 1.f : 0.f, 0.f)
-                        : make_float4(0.f, 0.f, 1.f, 0.f);
+    const bool live = G.state[slot] == 1;
+    const bool zero_az = !live || G.it[slot] == 0;  // fresh or empty slot: A z_0 = 0
+    G.prm[slot] = live ? make_float4(G.beta_cur[slot], G.inv_next[slot], zero_az ? 1.f : 0.f, 0.f)
+                       : make_float4(0.f, 0.f, 1.f, 0.f);
   };
   auto load_slot = [&](int j) {
     const int slot = slot0 + j;
-    const bool live = ss.state[slot] == 1;
-    const int src = ss.src[slot];
-    const int64_t u = live ? ss.unit[slot] : 0;
+    const bool live = G.state[slot] == 1;
+    const int src = G.src[slot];
+    const int64_t u = live ? G.unit[slot] : 0;
     float x = 0.f;
     if (live && grow < P.s) x = src >= 0 ? ring_x[(size_t)src * SL + lrow] : X[u * P.ldx + grow];
     xr[j] = x;
@@ -276,39 +328,26 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     lr[j] = 0.f;
   };
 
-  if (tid == 0) {
-    ss.head = 0; ss.tail = 0; ss.pf_from = 0; ss.pf_to = RING;
-    mbar_init(&ss.bar_p, 1);
-    mbar_init(&ss.bar_r, 1);
-    mbar_init(&ss.bar_a, 1);
-    mbar_init(&ss.bar_c, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) umma::tmem_alloc(&ss.tmem, TMEM_COLS);
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
-  const uint32_t tmem = ss.tmem;
+  if (gtid == 0) { G.head = 0; G.tail = 0; G.pf_from = 0; G.pf_to = RING; }
+  bar_sync(gbar, GT);
   prefetch();
   cp_async_wait_all();
-  __syncthreads();
-  if (tid == 0) {
-    ss.tail = RING;
-    for (int sl = 0; sl < TS; ++sl) { claim_into(sl); ss.finish[sl] = 0; }
-    ss.fmask = 0;
-    ss.pf_from = ss.tail;
-    ss.pf_to = ss.head + RING;
-    if (ss.pf_to < ss.pf_from) ss.pf_to = ss.pf_from;
+  bar_sync(gbar, GT);
+  if (gtid == 0) {
+    G.tail = RING;
+    for (int sl = 0; sl < TS; ++sl) claim_into(sl);
+    G.fmask = 0;
+    G.pf_from = G.tail;
+    G.pf_to = G.head + RING;
+    if (G.pf_to < G.pf_from) G.pf_to = G.pf_from;
   }
-  __syncthreads();
-  if (warp == 0) publish(lane);
+  bar_sync(gbar, GT);
+  if (gw == 0) publish(lane);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) load_slot(j);
-  umma::fence_async_smem();  // dictionary and zero z operands visible to the tensor core
-  __syncthreads();
-  if (tid == 0) ss.tail = ss.pf_to;
+  for (int j = 0; j < 16; ++j) load_slot(j);
+  bar_sync(gbar, GT);
+  if (gtid == 0) G.tail = G.pf_to;
   prefetch();
-  if (C > 1) cluster.sync();  // peers' mbarriers initialised before any DSMEM traffic
 
   // MMA descriptors (no swizzle): A K-major for phase a (LBO: next 8 columns, SBO: next 8 rows),
   // A MN-major for phase c (SBO: next 8 columns = M, LBO: next 8 rows = K); z and v MN-major
@@ -316,106 +355,42 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   const uint32_t a_addr = umma::saddr(aop), z_addr = umma::saddr(zop), v_addr = umma::saddr(vop);
   constexpr uint32_t ID_A = idesc_bf16(128, TS, 0, 1);
   constexpr uint32_t ID_C = idesc_bf16(128, TS, 1, 1);
+  const uint32_t bar_p = umma::saddr(&G.bar_p), bar_r = umma::saddr(&G.bar_r);
 
-  uint32_t phase = 0, ph_a = 0, ph_c = 0;
-  // fp32 z ping-pong: phase c of this pass writes (partial, then reduced) z_{it+1} into wbuf; the
-  // other buffer holds z_it, whose bf16 pieces phase a reads.  The decision at the start of the
-  // next pass outputs z of finished units from the buffer that pass is about to write (read
-  // before its phase c).
-  float* wbuf = zbuf0;
-  bool first = true;
-  const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0
-  long long tp[9];
+  uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
+  const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0, group 0
+  long long tp[8];
   auto stamp = [&](int i) { if (pf) tp[i] = clock64(); };
   for (;;) {
     stamp(0);
-    // ========== phase a on the tensor core: az = A_rows z  (z operand holds z_it); issued by warp 1
-    //            so that warp 0's decision runs while the MMAs are issued and executed
-    if (warp == 1 && lane == 0) {
+    // ========== phase a on the tensor core: az = A_rows z_it
+    if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll 1
       for (int ks = 0; ks < KP / 16; ++ks) {
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt) {
-          const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * Gm::a_piece * 2) + (uint32_t)(2 * ks) * 128u;
-          const uint32_t bb = z_addr + (uint32_t)(term_b(tt) * Gm::z_piece * 2) + (uint32_t)(2 * ks) * 512u;
+          const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * A_PIECE * 2) + (uint32_t)(2 * ks) * 128u;
+          const uint32_t bb = z_addr + (uint32_t)(term_b(tt) * Z_PIECE * 2) + (uint32_t)(2 * ks) * 512u;
           mma_bf16(tmem, umma::desc_noswz(aa, 128, KG * 128), umma::desc_noswz(bb, 512, 128), ID_A,
                    (ks | tt) != 0);
         }
       }
-      umma::commit(&ss.bar_a);
+      umma::commit(&G.bar_a);
     }
     __syncwarp();
-    // ========== warp 0: decision of the previous pass, outputs, refill claims (overlaps phase a)
-    if (warp == 0 && !first) {
-      const int slot = lane;
-      bool fin = false;
-      float r = 0.f;
-      for (int c = 0; c < C; ++c) r = fmaxf(r, rall[c * TS + slot]);
-      if (ss.state[slot] == 1) {
-        if (ss.it[slot] > 0) {
-          const float prev = ss.prev_res[slot];
-          const float rel = fabsf(r - prev) / fmaxf(r, Limits<float>::tiny());
-          ss.stalled[slot] = (rel < kStallEps) ? ss.stalled[slot] + 1 : 0;
-          ss.prev_res[slot] = r;
-          if (r <= ss.thresh[slot]) { fin = true; ss.code[slot] = L1F_UNIT_OK; }
-          else if (ss.stalled[slot] >= kStallIters) { fin = true; ss.code[slot] = L1F_UNIT_STALLED; }
-          else if (ss.it[slot] >= P.max_iter) { fin = true; ss.code[slot] = L1F_UNIT_MAXITER; }
-        }
-        if (!fin) {
-          ss.it[slot] += 1;
-          const float bc = ss.beta_next[slot];
-          ss.beta_cur[slot] = bc;
-          float bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
-          if (bn > ss.beta_max[slot]) bn = ss.beta_max[slot];
-          ss.beta_next[slot] = bn;
-          ss.inv_next[slot] = 1.f / bn;
-        }
-      }
-      ss.res[slot] = r;
-      ss.finish[slot] = fin;
-      const unsigned fmask = __ballot_sync(0xffffffffu, fin);
-      if (crank == 0) {  // the finished iteration's z is the previous pass's reduced z
-        const float* zprev = wbuf;  // z of the finished iteration (overwritten by this pass's phase c)
-        for (unsigned mm = fmask; mm; mm &= mm - 1) {
-          const int sl = __ffs(mm) - 1;
-          const int64_t u = ss.unit[sl];
-          for (int t = lane; t < P.k; t += 32) Z[u * P.ldz + t] = zprev[t * TSP + sl];
-          if (lane == 0) {
-            if (iters) iters[u] = ss.it[sl];
-            if (res_out) res_out[u] = ss.res[sl];
-            if (status) status[u] = ss.code[sl];
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
-        ss.pf_from = ss.tail > ss.head ? ss.tail : ss.head;
-        ss.pf_to = ss.head + RING;
-        ss.tail = ss.pf_to;
-        ss.fmask = fmask;
-      }
-      __syncwarp();
-      publish(lane);
-    }
-
-    // ========== az from TMEM
-    mbar_wait(&ss.bar_a, ph_a);
+    mbar_wait(&G.bar_a, ph_a);
     ph_a ^= 1;
-    stamp(1);
     umma::fence_after();
-    float az[8];
-    umma::ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0, az);
+    stamp(1);
+    float az[16];
+    umma::ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0, az);
     umma::ld_wait();
-    if (!__syncthreads_or(tid < TS && ss.state[tid] == 1)) break;
-    first = false;
-    stamp(2);
     {
-      const uint32_t fm = (ss.fmask >> slot0) & 0xFFu;
+      const uint32_t fm = (G.fmask >> slot0) & 0xFFFFu;
       if (fm) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 16; ++j)
           if (fm & (1u << j)) load_slot(j);
       }
     }
@@ -423,13 +398,13 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     // ========== phase b: elementwise ADM update (reformulated residual), v -> bf16 pieces
     if (E != nullptr && grow < P.s) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (ss.prm[slot0 + j].z == 0.f) E[(int64_t)ss.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
+      for (int j = 0; j < 16; ++j)
+        if (G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
     }
-    float rmax[8];
+    float rmax[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 pr = ss.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
+    for (int j = 0; j < 16; ++j) {
+      const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
       const float tn = pr.y;
       const float x = xr[j];
       const float azv = pr.z != 0.f ? 0.f : az[j];
@@ -445,173 +420,222 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       yr[j] = y;
     }
     // v operand: MN-major core matrices (row group rg, slot group sg) at (rg * 4 + sg) * 64
-    {
-      const size_t off = (size_t)((lrow >> 3) * 4 + h) * 64 + (lrow & 7) * 8;
-      split8_store(az, vop + off, vop + Gm::v_piece + off, vop + 2 * Gm::v_piece + off);
-    }
-    // per-slot max|r| over this warp's 32 rows: reduce-scatter butterfly (8 values over 32 lanes)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int hh = 0; hh < 2; ++hh) {
+      float v8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
+      const size_t off = (size_t)((lrow >> 3) * 4 + 2 * h + hh) * 64 + (lrow & 7) * 8;
+      split8_store(v8, vop + off, vop + V_PIECE + off, vop + 2 * V_PIECE + off);
+    }
+    // per-slot max|r| over this warp's 32 rows: reduce-scatter butterfly (16 values over 32 lanes)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
       const bool up = lane & 16;
-      const float send = up ? rmax[i] : rmax[i + 4];
-      const float keep = up ? rmax[i + 4] : rmax[i];
+      const float send = up ? rmax[i] : rmax[i + 8];
+      const float keep = up ? rmax[i + 8] : rmax[i];
       rmax[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 16));
     }
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const bool up = lane & 8;
-      const float send = up ? rmax[i] : rmax[i + 2];
-      const float keep = up ? rmax[i + 2] : rmax[i];
+      const float send = up ? rmax[i] : rmax[i + 4];
+      const float keep = up ? rmax[i + 4] : rmax[i];
       rmax[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
     }
-    {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
       const bool up = lane & 4;
+      const float send = up ? rmax[i] : rmax[i + 2];
+      const float keep = up ? rmax[i + 2] : rmax[i];
+      rmax[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+    }
+    {
+      const bool up = lane & 2;
       const float send = up ? rmax[0] : rmax[1];
       const float keep = up ? rmax[1] : rmax[0];
-      rmax[0] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 4));
-      rmax[0] = fmaxf(rmax[0], __shfl_xor_sync(0xffffffffu, rmax[0], 2));
+      rmax[0] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 2));
       rmax[0] = fmaxf(rmax[0], __shfl_xor_sync(0xffffffffu, rmax[0], 1));
     }
-    // lane holds slot slot0 + 4 b4 + 2 b3 + b2 (bits of the lane)
-    if ((lane & 3) == 0) rpart[q * TS + slot0 + (lane >> 2)] = rmax[0];
+    // lane holds slot slot0 + 8 b4 + 4 b3 + 2 b2 + b1 (bits of the lane)
+    if ((lane & 1) == 0) rpart[q * TS + slot0 + (lane >> 1)] = rmax[0];
     umma::fence_async_smem();
     umma::fence_before();
-    __syncthreads();
+    bar_sync(gbar, GT);
+    stamp(2);
 
-    stamp(3);
     // ========== phase c on the tensor core: zp = A_rows^T v
-    if (warp == 1 && lane == 0) {
+    if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll 1
       for (int ks = 0; ks < SL / 16; ++ks) {
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt) {
-          const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * Gm::a_piece * 2) + (uint32_t)(2 * ks) * (KG * 128u);
-          const uint32_t bb = v_addr + (uint32_t)(term_b(tt) * Gm::v_piece * 2) + (uint32_t)(2 * ks) * 512u;
+          const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * A_PIECE * 2) + (uint32_t)(2 * ks) * (KG * 128u);
+          const uint32_t bb = v_addr + (uint32_t)(term_b(tt) * V_PIECE * 2) + (uint32_t)(2 * ks) * 512u;
           mma_bf16(tmem + 32, umma::desc_noswz(aa, KG * 128, 128), umma::desc_noswz(bb, 512, 128), ID_C,
                    (ks | tt) != 0);
         }
       }
-      umma::commit(&ss.bar_c);
+      umma::commit(&G.bar_c);
     }
     __syncwarp();
-    prefetch();  // ring entries claimed above were consumed by load_slot
-    if (tid < TS) {  // CTA-local max|r| per slot
-      float m = fmaxf(fmaxf(rpart[tid], rpart[TS + tid]), fmaxf(rpart[2 * TS + tid], rpart[3 * TS + tid]));
-      rall[crank * TS + tid] = m;
+    prefetch();  // ring entries claimed by the last decision were consumed by load_slot
+    float* rall_p = rall + (size_t)par * C * TS;
+    if (C > 1 && gtid == 0) {
+      mbar_arm(&G.bar_p, (uint32_t)((C - 1) * (vmine * TS * 4 + TS * 4)));
+      uint32_t br = 0;
+      for (int c = 0; c < C; ++c)
+        if (c != crank) br += (uint32_t)max(0, min(rs, KP - c * rs)) * 192u;
+      mbar_arm(&G.bar_r, br);
     }
-    mbar_wait(&ss.bar_c, ph_c);
+    if (gw == 0) {  // CTA-local max|r| per slot -> every CTA (round 1)
+      const float m = fmaxf(fmaxf(rpart[lane], rpart[TS + lane]), fmaxf(rpart[2 * TS + lane], rpart[3 * TS + lane]));
+      rall_p[crank * TS + lane] = m;
+      __syncwarp();
+      if (C > 1)
+        for (int idx = lane; idx < (C - 1) * (TS / 4); idx += 32) {
+          const int d = idx / (TS / 4), ch = idx - d * (TS / 4);
+          const int peer = d < crank ? d : d + 1;
+          const float* src = rall_p + crank * TS + 4 * ch;
+          st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar_p, peer));
+        }
+    }
+    mbar_wait(&G.bar_c, ph_c);
     ph_c ^= 1;
-    stamp(4);
     umma::fence_after();
-    {
-      float zp[8];
-      umma::ld8(tmem + ((uint32_t)(32 * q) << 16) + 32u + (uint32_t)slot0, zp);
+    stamp(3);
+    {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
+      float zp[16];
+      umma::ld16(tmem + ((uint32_t)(32 * q) << 16) + 32u + (uint32_t)slot0, zp);
       umma::ld_wait();
-      const int t = lrow;  // TMEM lane = dictionary column
+      const int t = lrow;
       if (t < KP) {
-        float* dst = wbuf + (size_t)t * TSP + slot0;
-        *reinterpret_cast<float4*>(dst) = make_float4(zp[0], zp[1], zp[2], zp[3]);
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(zp[4], zp[5], zp[6], zp[7]);
+        const int owner = t / rs, row = t - owner * rs;
+        float* dst = zin + (size_t)(crank * rs + row) * TSP + slot0;
+        if (owner == crank) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<float4*>(dst + 4 * i) = make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
+        } else {
+          const uint32_t pdst = peer_addr(umma::saddr(dst), owner), pbar = peer_addr(bar_p, owner);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) st_async16v(pdst + 16 * i, zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3], pbar);
+        }
       }
     }
     umma::fence_before();
-    __syncthreads();
+    if (C > 1) mbar_wait(&G.bar_p, ph_x);
+    bar_sync(gbar, GT);  // local rows of zp and rall_p[crank] written
+    stamp(4);
 
-    stamp(5);
-    // ========== cluster reduction: partial slices -> owners, reduced slices + max|r| -> all
-    if (C > 1) {
-      const int slice_chunks = rs * TSP / 4;
-      const uint32_t bar_p = umma::saddr(&ss.bar_p), bar_r = umma::saddr(&ss.bar_r);
-      if (tid == 0) {
-        mbar_arm(&ss.bar_p, (uint32_t)((C - 1) * rs * TSP * 4));
-        uint32_t br = 0;
-        for (int c = 0; c < C; ++c) {
-          if (c == crank) continue;
-          const int vc = max(0, min(rs, KP - c * rs));
-          br += (uint32_t)(vc * 192 + TS * 4 + (crank == 0 ? vc * 128 : 0));
+    float* zs_cur = zsl + (size_t)par * rs * TS;         // z_{it+1} slice (this pass)
+    float* zs_prev = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
+    if (gw == 0) {
+      // ========== decision (l1reg.py:100-128) from the global max|r_it|; outputs of finished units
+      const int slot = lane;
+      bool fin = false;
+      float r = 0.f;
+      for (int c = 0; c < C; ++c) r = fmaxf(r, rall_p[c * TS + slot]);
+      if (G.state[slot] == 1) {
+        if (G.it[slot] > 0) {
+          const float prev = G.prev_res[slot];
+          const float rel = fabsf(r - prev) / fmaxf(r, Limits<float>::tiny());
+          G.stalled[slot] = (rel < kStallEps) ? G.stalled[slot] + 1 : 0;
+          G.prev_res[slot] = r;
+          uint8_t code = 0xFF;
+          if (r <= G.thresh[slot]) code = L1F_UNIT_OK;
+          else if (G.stalled[slot] >= kStallIters) code = L1F_UNIT_STALLED;
+          else if (G.it[slot] >= P.max_iter) code = L1F_UNIT_MAXITER;
+          if (code != 0xFF) {
+            fin = true;
+            if (crank == 0) {
+              const int64_t u = G.unit[slot];
+              if (iters) iters[u] = G.it[slot];
+              if (res_out) res_out[u] = r;
+              if (status) status[u] = code;
+            }
+          }
         }
-        mbar_arm(&ss.bar_r, br);
+        if (!fin) {
+          G.it[slot] += 1;
+          const float bc = G.beta_next[slot];
+          G.beta_cur[slot] = bc;
+          float bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
+          if (bn > G.beta_max[slot]) bn = G.beta_max[slot];
+          G.beta_next[slot] = bn;
+          G.inv_next[slot] = 1.f / bn;
+        }
       }
-      for (int idx = tid; idx < (C - 1) * slice_chunks; idx += NT) {
-        const int d = idx / slice_chunks, ch = idx - d * slice_chunks;
-        const int owner = d < crank ? d : d + 1;
-        const float* src = wbuf + (size_t)owner * rs * TSP + (size_t)ch * 4;
-        const uint32_t dst = peer_addr(umma::saddr(zin + (size_t)crank * rs * TSP + (size_t)ch * 4), owner);
-        st_async16(dst, src, peer_addr(bar_p, owner));
+      const unsigned fmask = __ballot_sync(0xffffffffu, fin);
+      for (unsigned mm = fmask; mm; mm &= mm - 1) {  // my slice of z_it of every finished unit
+        const int sl = __ffs(mm) - 1;
+        const int64_t u = G.unit[sl];
+        for (int row = lane; row < vmine; row += 32)
+          if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zs_prev[row * TS + sl];
       }
-      mbar_wait(&ss.bar_p, phase);
-      // owner: sum my slice of z_{it+1} (fp32 into wbuf for rank 0's outputs) and split it into the
-      // bf16 pieces of the phase-a operand; then push the pieces to every peer's z operand, the
-      // fp32 slice to rank 0, and my per-slot max|r| to every peer
-      const int r0 = crank * rs;
-      const int vmine = max(0, min(rs, KP - r0));
-      for (int e = tid; e < vmine * 4; e += NT) {
+      __syncwarp();
+      if (lane == 0) {
+        for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
+        G.pf_from = G.tail > G.head ? G.tail : G.head;
+        G.pf_to = G.head + RING;
+        G.tail = G.pf_to;
+        G.fmask = fmask;
+      }
+      __syncwarp();
+      publish(lane);
+    } else {
+      // ========== round 2: sum my slice, split into bf16 pieces, push the pieces to every CTA
+      const int gt2 = gtid - 32;
+      for (int e = gt2; e < vmine * 4; e += GT - 32) {
         const int row = e >> 2, sg = e & 3, t = r0 + row;
         float v8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = 0.f;
         for (int c = 0; c < C; ++c) {
-          const float* src = (c == crank) ? wbuf + (size_t)t * TSP + 8 * sg : zin + ((size_t)c * rs + row) * TSP + 8 * sg;
+          const float* src = zin + (size_t)(c * rs + row) * TSP + 8 * sg;
           const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
           v8[0] += a.x; v8[1] += a.y; v8[2] += a.z; v8[3] += a.w;
           v8[4] += b.x; v8[5] += b.y; v8[6] += b.z; v8[7] += b.w;
         }
-        float* dst = wbuf + (size_t)t * TSP + 8 * sg;
-        *reinterpret_cast<float4*>(dst) = make_float4(v8[0], v8[1], v8[2], v8[3]);
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
+        float* dz = zs_cur + (size_t)row * TS + 8 * sg;
+        *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
+        *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
         const size_t off = (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
-        split8_store(v8, zop + off, zop + Gm::z_piece + off, zop + 2 * Gm::z_piece + off);
+        split8_store(v8, zop + off, zop + Z_PIECE + off, zop + 2 * Z_PIECE + off);
       }
-      __syncthreads();
-      const int pc = vmine * 12, fc = vmine * 8, npush = pc + TS / 4 + fc;
-      for (int idx = tid; idx < (C - 1) * npush; idx += NT) {
-        const int d = idx / npush, ch = idx - d * npush;
-        const int peer = d < crank ? d : d + 1;
-        const void* src;
-        uint32_t bar = bar_r;
-        if (ch < pc) {  // bf16 piece chunk: (piece, row, slot group)
+      if (C > 1) {
+        bar_sync(sbar, GT - 32);
+        const int pc = vmine * 12;
+        for (int idx = gt2; idx < (C - 1) * pc; idx += GT - 32) {
+          const int d = idx / pc, ch = idx - d * pc;
+          const int peer = d < crank ? d : d + 1;
           const int piece = ch / (vmine * 4), rem = ch - piece * vmine * 4;
           const int t = r0 + (rem >> 2), sg = rem & 3;
-          src = zop + (size_t)piece * Gm::z_piece + (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
-        } else if (ch < pc + TS / 4) {
-          src = rall + (size_t)crank * TS + (size_t)(ch - pc) * 4;
-        } else {
-          if (peer != 0) continue;
-          const int fch = ch - pc - TS / 4;
-          src = wbuf + (size_t)(r0 + (fch >> 3)) * TSP + (size_t)(fch & 7) * 4;
+          const __nv_bfloat16* src = zop + (size_t)piece * Z_PIECE + (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
+          st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar_r, peer));
         }
-        st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar, peer));
-      }
-      mbar_wait(&ss.bar_r, phase);
-      phase ^= 1;
-    } else {
-      for (int e = tid; e < KP * (TS / 8); e += NT) {
-        const int t = e >> 2, sg = e & 3;
-        const float* src = wbuf + (size_t)t * TSP + 8 * sg;
-        const float4 lo = *reinterpret_cast<const float4*>(src), hi = *reinterpret_cast<const float4*>(src + 4);
-        const float v8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        const size_t off = (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
-        split8_store(v8, zop + off, zop + Gm::z_piece + off, zop + 2 * Gm::z_piece + off);
       }
     }
-    stamp(6);
+    stamp(5);
+    if (C > 1) mbar_wait(&G.bar_r, ph_x);
+    ph_x ^= 1;
+    par ^= 1;
     cp_async_wait_all();
     umma::fence_async_smem();
     umma::fence_before();
-    __syncthreads();  // z operand, reduced z, rall and the prefetched ring visible to all
-    stamp(7);
-    wbuf = (wbuf == zbuf0) ? zbuf1 : zbuf0;
-    stamp(8);
+    const bool any = bar_or(gbar, GT, gtid < TS && G.state[gtid] == 1);
+    stamp(6);
     if (pf) {
-      for (int i = 1; i < 9; ++i) prof[i] += tp[i] - tp[i - 1];
+      for (int i = 1; i < 7; ++i) prof[i] += tp[i] - tp[i - 1];
       prof[0] += 1;
     }
+    if (!any) break;
   }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  if (warp == 0) umma::tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 0) umma::tmem_dealloc(tmem_base, TMEM_COLS);
   if (C > 1) cluster.sync();
 }
 
@@ -641,19 +665,28 @@ __global__ void unit_scale_kernel(const float* __restrict__ X, Params P, float* 
   }
 }
 
+constexpr uint32_t kSmemLimit = 227u * 1024u - 6144u;  // dynamic budget next to the static Group state
+
+template <int KP>
+bool fits(int s) {
+  const int C = (int)ceil_div(s, SL);
+  return make_layout<KP>(C, (int)ceil_div(KP, C)).total <= kSmemLimit;
+}
+
 template <int KP>
 int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k, double tol,
            double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz, float* E, int64_t lde,
            int32_t* iters, float* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st, bool query,
            size_t* need) {
-  using Gm = Geo<KP>;
   const int C = (int)ceil_div(s, SL);
+  const int rs = (int)ceil_div(KP, C);
+  const Layout Lo = make_layout<KP>(C, rs);
   const size_t scale_bytes = (sizeof(float) * (size_t)(n_units > 0 ? n_units : 1) + 255) & ~(size_t)255;
   if (query) { *need = scale_bytes; return L1F_OK; }
   auto kern = adm_tc_kernel<KP>;
   static bool configured = false;
   if (!configured) {
-    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::smem_bytes));
+    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
@@ -665,7 +698,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     L1F_REQUIRE(ws_bytes >= scale_bytes, L1F_ERR_ARG, "filter: workspace too small");
   }
   Params P;
-  P.s = s; P.k = k; P.cluster = C; P.rs = (int)ceil_div(KP, C);
+  P.s = s; P.k = k; P.cluster = C; P.rs = rs;
   P.n_units = n_units; P.ldx = ldx; P.ldz = ldz; P.lde = lde; P.max_iter = max_iter;
   P.tol = tol; P.rho = rho; P.beta0 = beta0; P.beta_max = beta_max;
   float* scale = (float*)workspace;
@@ -681,7 +714,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(NT, 1, 1);
-    cfg.dynamicSmemBytes = Gm::smem_bytes;
+    cfg.dynamicSmemBytes = Lo.total;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -689,7 +722,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     int max_clusters = 0;
     if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
       max_clusters = std::max(1, num_sms() / C);
-    const int64_t want = ceil_div(n_units, TS);
+    const int64_t want = ceil_div(n_units, (int64_t)TS * NG);
     const int nclusters = (int)std::min<int64_t>(max_clusters, std::max<int64_t>(1, want));
     cfg.gridDim = dim3((unsigned)(nclusters * C), 1, 1);
     static long long* prof = nullptr;
@@ -698,13 +731,12 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
       cudaMallocManaged(&prof, 16 * sizeof(long long));
       memset(prof, 0, 16 * sizeof(long long));
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Z, E, iters, res, status, prof);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof);
     if (prof) {
       cudaStreamSynchronize(st);
-      const char* names[9] = {"passes", "a:mma+decision", "syncthreads_or", "phase b", "c:mma wait", "zp->smem",
-                              "reduction", "cp wait+sync", "convert"};
-      fprintf(stderr, "[tc prof] KP=%d C=%d", KP, C);
-      for (int i = 0; i < 9; ++i)
+      const char* names[7] = {"passes", "a:mma", "phase b", "c:mma", "round1", "decide+round2", "round2 wait"};
+      fprintf(stderr, "[tc prof] KP=%d C=%d clusters=%d smem=%u", KP, C, nclusters, Lo.total);
+      for (int i = 0; i < 7; ++i)
         fprintf(stderr, " %s=%.0f", names[i], i ? (double)prof[i] / (double)prof[0] : (double)prof[0]);
       fprintf(stderr, "\n");
       memset(prof, 0, 16 * sizeof(long long));
@@ -735,6 +767,7 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
   if (k <= 16 || kp > 128 || s > 16 * l1f::tcf::SL) return L1F_ERR_UNSUPPORTED;
 #define L1F_TC(KP)                                                                                               \
   case KP:                                                                                                       \
+    if (!l1f::tcf::fits<KP>(s)) return L1F_ERR_UNSUPPORTED;                                                      \
     return l1f::tcf::launch<KP>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, \
                                 iters, res, status, workspace, ws_bytes, st, query, need)
   switch (kp) {
