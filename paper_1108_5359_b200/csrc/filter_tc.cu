@@ -157,25 +157,40 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16& p0, __nv_bfloat16
   p1 = __float2bfloat16_rn(r1);
   p2 = __float2bfloat16_rn(r1 - __bfloat162float(p1));
 }
-__device__ __forceinline__ uint32_t pack2(__nv_bfloat16 lo, __nv_bfloat16 hi) {
-  return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+// two fp32 -> packed bf16x2 (round to nearest) and back
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
-// 8 consecutive fp32 -> three 16-byte rows of bf16 pieces
-__device__ __forceinline__ void split8_store(const float (&v)[8], __nv_bfloat16* d0, __nv_bfloat16* d1,
-                                             __nv_bfloat16* d2) {
-  uint32_t w0[4], w1[4], w2[4];
+__device__ __forceinline__ float bf_lo(uint32_t p) { return __uint_as_float(p << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
+// 8 consecutive fp32 -> the three bf16 pieces as 16-byte rows (same rounding as split3)
+__device__ __forceinline__ void split8(const float (&v)[8], uint4& w0, uint4& w1, uint4& w2) {
+  uint32_t a[4], b[4], c[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __nv_bfloat16 a0, a1, a2, b0, b1, b2;
-    split3(v[2 * i], a0, a1, a2);
-    split3(v[2 * i + 1], b0, b1, b2);
-    w0[i] = pack2(a0, b0);
-    w1[i] = pack2(a1, b1);
-    w2[i] = pack2(a2, b2);
+    const float x0 = v[2 * i], x1 = v[2 * i + 1];
+    a[i] = cvt_bf16x2(x0, x1);
+    const float r0 = x0 - bf_lo(a[i]), r1 = x1 - bf_hi(a[i]);
+    b[i] = cvt_bf16x2(r0, r1);
+    c[i] = cvt_bf16x2(r0 - bf_lo(b[i]), r1 - bf_hi(b[i]));
   }
-  *reinterpret_cast<uint4*>(d0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-  *reinterpret_cast<uint4*>(d1) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-  *reinterpret_cast<uint4*>(d2) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+  w0 = make_uint4(a[0], a[1], a[2], a[3]);
+  w1 = make_uint4(b[0], b[1], b[2], b[3]);
+  w2 = make_uint4(c[0], c[1], c[2], c[3]);
+}
+__device__ __forceinline__ void split8_store(const float (&v)[8], __nv_bfloat16* d0, __nv_bfloat16* d1,
+                                             __nv_bfloat16* d2) {
+  uint4 w0, w1, w2;
+  split8(v, w0, w1, w2);
+  *reinterpret_cast<uint4*>(d0) = w0;
+  *reinterpret_cast<uint4*>(d1) = w1;
+  *reinterpret_cast<uint4*>(d2) = w2;
+}
+__device__ __forceinline__ void st_async16u(uint32_t peer_dst, uint4 v, uint32_t peer_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(peer_dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(peer_bar) : "memory");
 }
 
 // products (i, j) of the 3-piece split kept: i + j <= 2
@@ -359,7 +374,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 
   uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
   const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0, group 0
-  long long tp[8];
+  long long tp[10];
   auto stamp = [&](int i) { if (pf) tp[i] = clock64(); };
   for (;;) {
     stamp(0);
@@ -525,9 +540,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       }
     }
     umma::fence_before();
+    stamp(4);
     if (C > 1) mbar_wait(&G.bar_p, ph_x);
     bar_sync(gbar, GT);  // local rows of zp and rall_p[crank] written
-    stamp(4);
+    stamp(5);
 
     float* zs_cur = zsl + (size_t)par * rs * TS;         // z_{it+1} slice (this pass)
     float* zs_prev = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
@@ -585,39 +601,67 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       __syncwarp();
       publish(lane);
     } else {
-      // ========== round 2: sum my slice, split into bf16 pieces, push the pieces to every CTA
+      // ========== round 2: sum my slice, split into bf16 pieces, push the pieces to every CTA.
+      // Item (row, 8-slot group) is handled by nrep threads; each sums it (cheap, redundant) and
+      // pushes the pieces from registers to every nrep-th peer; replica 0 also stores locally.
       const int gt2 = gtid - 32;
-      for (int e = gt2; e < vmine * 4; e += GT - 32) {
-        const int row = e >> 2, sg = e & 3, t = r0 + row;
+      const int nitems = vmine * 4;
+      const int nrep = nitems > 0 ? max(1, (GT - 32) / nitems) : 1;
+      const int item = gt2 % max(nitems, 1), rep = gt2 / max(nitems, 1);
+      if (nitems > 0 && rep < nrep) {
+        const int row = item >> 2, sg = item & 3, t = r0 + row;
         float v8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = 0.f;
-        for (int c = 0; c < C; ++c) {
-          const float* src = zin + (size_t)(c * rs + row) * TSP + 8 * sg;
-          const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
-          v8[0] += a.x; v8[1] += a.y; v8[2] += a.z; v8[3] += a.w;
-          v8[4] += b.x; v8[5] += b.y; v8[6] += b.z; v8[7] += b.w;
+        {  // fixed summation order c = 0 .. C-1 (results independent of the unrolling)
+          const float* src0 = zin + (size_t)row * TSP + 8 * sg;
+          const size_t cstride = (size_t)rs * TSP;
+          int c = 0;
+          for (; c + 4 <= C; c += 4) {
+            float4 a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              a[u] = *reinterpret_cast<const float4*>(src0 + (c + u) * cstride);
+              b[u] = *reinterpret_cast<const float4*>(src0 + (c + u) * cstride + 4);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              v8[0] += a[u].x; v8[1] += a[u].y; v8[2] += a[u].z; v8[3] += a[u].w;
+              v8[4] += b[u].x; v8[5] += b[u].y; v8[6] += b[u].z; v8[7] += b[u].w;
+            }
+          }
+          for (; c < C; ++c) {
+            const float4 a = *reinterpret_cast<const float4*>(src0 + c * cstride);
+            const float4 b = *reinterpret_cast<const float4*>(src0 + c * cstride + 4);
+            v8[0] += a.x; v8[1] += a.y; v8[2] += a.z; v8[3] += a.w;
+            v8[4] += b.x; v8[5] += b.y; v8[6] += b.z; v8[7] += b.w;
+          }
         }
-        float* dz = zs_cur + (size_t)row * TS + 8 * sg;
-        *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
-        *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
+        stamp(7);
+        uint4 w0, w1, w2;
+        split8(v8, w0, w1, w2);
         const size_t off = (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
-        split8_store(v8, zop + off, zop + Z_PIECE + off, zop + 2 * Z_PIECE + off);
-      }
-      if (C > 1) {
-        bar_sync(sbar, GT - 32);
-        const int pc = vmine * 12;
-        for (int idx = gt2; idx < (C - 1) * pc; idx += GT - 32) {
-          const int d = idx / pc, ch = idx - d * pc;
+        stamp(8);
+        if (rep == 0) {
+          float* dz = zs_cur + (size_t)row * TS + 8 * sg;
+          *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
+          *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
+          *reinterpret_cast<uint4*>(zop + off) = w0;
+          *reinterpret_cast<uint4*>(zop + Z_PIECE + off) = w1;
+          *reinterpret_cast<uint4*>(zop + 2 * Z_PIECE + off) = w2;
+        }
+        const uint32_t a0 = umma::saddr(zop + off), a1 = umma::saddr(zop + Z_PIECE + off),
+                       a2 = umma::saddr(zop + 2 * Z_PIECE + off);
+        for (int d = rep; d < C - 1; d += nrep) {
           const int peer = d < crank ? d : d + 1;
-          const int piece = ch / (vmine * 4), rem = ch - piece * vmine * 4;
-          const int t = r0 + (rem >> 2), sg = rem & 3;
-          const __nv_bfloat16* src = zop + (size_t)piece * Z_PIECE + (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
-          st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar_r, peer));
+          const uint32_t pb = peer_addr(bar_r, peer);
+          st_async16u(peer_addr(a0, peer), w0, pb);
+          st_async16u(peer_addr(a1, peer), w1, pb);
+          st_async16u(peer_addr(a2, peer), w2, pb);
         }
       }
+      stamp(9);
     }
-    stamp(5);
     if (C > 1) mbar_wait(&G.bar_r, ph_x);
     ph_x ^= 1;
     par ^= 1;
@@ -627,7 +671,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     const bool any = bar_or(gbar, GT, gtid < TS && G.state[gtid] == 1);
     stamp(6);
     if (pf) {
-      for (int i = 1; i < 7; ++i) prof[i] += tp[i] - tp[i - 1];
+      const int order[10] = {0, 1, 2, 3, 4, 5, 7, 8, 9, 6};
+      for (int i = 1; i < 10; ++i) prof[i] += tp[order[i]] - tp[order[i - 1]];
       prof[0] += 1;
     }
     if (!any) break;
@@ -734,9 +779,9 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof);
     if (prof) {
       cudaStreamSynchronize(st);
-      const char* names[7] = {"passes", "a:mma", "phase b", "c:mma", "round1", "decide+round2", "round2 wait"};
+      const char* names[10] = {"passes", "a:mma", "phase b", "c:mma", "ld+push1", "wait1", "sumloop", "split", "store+push2", "wait2+bar_or"};
       fprintf(stderr, "[tc prof] KP=%d C=%d clusters=%d smem=%u", KP, C, nclusters, Lo.total);
-      for (int i = 0; i < 7; ++i)
+      for (int i = 0; i < 10; ++i)
         fprintf(stderr, " %s=%.0f", names[i], i ? (double)prof[i] / (double)prof[0] : (double)prof[0]);
       fprintf(stderr, "\n");
       memset(prof, 0, 16 * sizeof(long long));
