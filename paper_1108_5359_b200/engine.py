@@ -280,6 +280,111 @@ def solve_from_seed(mt, plan, l_out=None, s_out=None):
     return f
 
 
+class HostPipeline:
+    """solve_from_seed for M, L and S in pinned host memory, with the PCIe traffic overlapped.
+
+    The column panel is gathered straight from the pinned host matrix (zero-copy through UVA,
+    ~s_r * n * 4 bytes) so the column filter starts at once; meanwhile M is copied to the device
+    in row chunks on a copy stream.  As each chunk lands: its row panel, its row units'
+    filter, its rows of Af, and L, S = M - L for its rows; those go back on a second copy stream
+    while the next chunks compute.  The device->host copy of L and S (2 x 4 bytes per entry)
+    is the floor.  Everything chunk-specific (index tensors, factor slices) is prepared here so
+    the host never blocks while enqueueing a solve.
+    """
+
+    def __init__(self, plan, n_chunks=8):
+        if plan.row_range != (0, plan.m_rows) or len(plan.comp_cols) != len(plan.comp_cols_all):
+            raise ValueError("HostPipeline needs a single-GPU plan over the whole matrix")
+        self.plan = plan
+        m, n, k = plan.m_rows, plan.m_cols, plan.k
+        dt, fdt = plan.dtype, plan.filter_dtype
+        seed = plan.seed
+        self.m_dev = torch.empty((m, n), dtype=dt, device="cuda")
+        self.l_dev = torch.empty((m, n), dtype=dt, device="cuda")
+        self.s_dev = torch.empty((m, n), dtype=dt, device="cuda")
+        self.xc = torch.empty((len(plan.comp_cols), len(seed.row_idx)), dtype=fdt, device="cuda")
+        self.zr = torch.empty((len(plan.comp_rows_all), k), dtype=fdt, device="cuda")
+        self.bf = torch.empty((n, k), dtype=dt, device="cuda")
+        self.rs = torch.zeros((n_chunks, 2), dtype=torch.float64, device="cuda")
+        self.h2d, self.d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        bounds = np.linspace(0, m, n_chunks + 1).astype(np.int64)
+        comp_rows = plan.comp_rows_all
+        self.chunks = []
+        for i, (r0, r1) in enumerate(zip(bounds[:-1], bounds[1:])):
+            r0, r1 = int(r0), int(r1)
+            u0, u1 = np.searchsorted(comp_rows, [r0, r1])
+            loc = (seed.row_idx >= r0) & (seed.row_idx < r1)
+            c = dict(r0=r0, r1=r1, u0=int(u0), u1=int(u1),
+                     d_rows=index_tensor(comp_rows[u0:u1]),
+                     d_seed_rows=index_tensor(seed.row_idx[loc] - r0), n_seed=int(loc.sum()),
+                     u_local=seed.u[index_tensor(np.flatnonzero(loc))].contiguous(),
+                     xr=torch.empty((int(u1 - u0), len(seed.col_idx)), dtype=fdt, device="cuda"),
+                     af=torch.empty((r1 - r0, k), dtype=dt, device="cuda"),
+                     ev_h=torch.cuda.Event(), ev_c=torch.cuda.Event())
+            self.chunks.append(c)
+        self.ev_start, self.ev_d2h = torch.cuda.Event(), torch.cuda.Event()
+
+    def solve(self, m_host, l_host, s_host):
+        """Enqueue one solve; returns (filter stats dict, residual partials).  The caller's
+        stream waits for the last device->host copy."""
+        from .l1reg import filter_units
+        p, seed = self.plan, self.plan.seed
+        comp = torch.cuda.current_stream()
+        code_in = dv.dtype_code(self.m_dev)
+        code_f = _lib.F32 if p.filter_dtype == torch.float32 else _lib.F64
+        self.ev_start.record(comp)
+        self.h2d.wait_event(self.ev_start)
+        self.d2h.wait_event(self.ev_start)
+        # H2D of the row chunks (copy engine)
+        with torch.cuda.stream(self.h2d):
+            for c in self.chunks:
+                self.m_dev[c["r0"]:c["r1"]].copy_(m_host[c["r0"]:c["r1"]], non_blocking=True)
+                c["ev_h"].record(self.h2d)
+        # column panel straight from host memory, column filter
+        _lib.call("l1f_gather", code_in, m_host.data_ptr(), m_host.stride(0), dv.ptr(p.d_row_idx),
+                  len(seed.row_idx), dv.ptr(p.d_comp_cols), len(p.comp_cols), code_f, dv.ptr(self.xc),
+                  self.xc.stride(0), 1, dv.stream())
+        zc, _, itc, _, stc = filter_units(self.xc, p.u, p.adm, want_e=False, workspace=p.workspace)
+        if p.filter_dtype != p.dtype:
+            zc = zc.to(p.dtype)
+        k = p.k
+        code = _lib.F32 if p.dtype == torch.float32 else _lib.F64
+        its, sts = [], []
+        for i, c in enumerate(self.chunks):
+            comp.wait_event(c["ev_h"])
+            nu = c["u1"] - c["u0"]
+            if nu:
+                _lib.call("l1f_gather", code_in, dv.ptr(self.m_dev), self.m_dev.stride(0), dv.ptr(c["d_rows"]), nu,
+                          dv.ptr(p.d_col_idx), len(seed.col_idx), code_f, dv.ptr(c["xr"]), c["xr"].stride(0), 0,
+                          dv.stream())
+                zr, _, itr, _, st_r = filter_units(c["xr"], p.v, p.adm, want_e=False, workspace=p.workspace)
+                its.append(itr)
+                sts.append(st_r)
+                if p.filter_dtype != p.dtype:
+                    zr = zr.to(p.dtype)
+            else:
+                zr = self.zr[:0]
+            rows = c["r1"] - c["r0"]
+            _lib.call("l1f_build_factors", code, rows, p.m_cols, k, dv.ptr(c["d_seed_rows"]), c["n_seed"],
+                      dv.ptr(p.d_col_idx), len(seed.col_idx), dv.ptr(c["u_local"]), dv.ptr(seed.sigma),
+                      dv.ptr(seed.v), dv.ptr(zc), zc.stride(0), dv.ptr(zr), max(zr.stride(0), k), dv.ptr(c["af"]),
+                      dv.ptr(self.bf), dv.stream())
+            md, ld, sd = self.m_dev[c["r0"]:c["r1"]], self.l_dev[c["r0"]:c["r1"]], self.s_dev[c["r0"]:c["r1"]]
+            _lib.call("l1f_reconstruct", code_in, rows, p.m_cols, k, dv.ptr(c["af"]), k, dv.ptr(self.bf), k,
+                      dv.ptr(md), md.stride(0), dv.ptr(ld), ld.stride(0), dv.ptr(sd), sd.stride(0),
+                      dv.ptr(self.rs[i]), dv.stream())
+            c["ev_c"].record(comp)
+            self.d2h.wait_event(c["ev_c"])
+            with torch.cuda.stream(self.d2h):
+                l_host[c["r0"]:c["r1"]].copy_(ld, non_blocking=True)
+                s_host[c["r0"]:c["r1"]].copy_(sd, non_blocking=True)
+        self.ev_d2h.record(self.d2h)
+        comp.wait_event(self.ev_d2h)
+        itr = torch.cat(its) if its else torch.zeros(0, dtype=torch.int32, device="cuda")
+        st_r = torch.cat(sts) if sts else torch.zeros(0, dtype=torch.uint8, device="cuda")
+        return dict(iters_c=itc, iters_r=itr, status_c=stc, status_r=st_r), self.rs.sum(dim=0)
+
+
 # ------------------------------------------------------------------ synthetic inputs
 def generate_matrix(m, n, r, rho_s, magnitude, seed=0, kind=_lib.GEN_GAUSSIAN, row0=0, rows=None,
                     want_l0=False, out=None):
