@@ -206,72 +206,114 @@ template <> struct Vec4g<double> {
   }
 };
 
+// Streaming reconstruction for small k (K4, k <= 16): each CTA owns a 1024-column strip (8 warps x
+// 128 columns, 4 per thread: 4 KB contiguous per row for the DRAM) and walks a range of rows, RPT
+// rows per step, keeping its Bf columns in registers; the A rows are broadcast loads shared by the
+// 8 warps; the next step's M is in flight while the current one computes.  12 B of DRAM traffic
+// per entry (M in, L and S out).  The residual partial of (M - L) - S is identically 0 (S is
+// stored as the fp32 value of M - L, as the reference's s = m - l), so only sum(M^2) is kept.
+template <typename T> struct Vec4s;
+template <> struct Vec4s<float> {
+  __device__ static __forceinline__ void ld(const float* p, float* v) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+};
+template <> struct Vec4s<double> {
+  __device__ static __forceinline__ void ld(const double* p, double* v) {
+    const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+constexpr int kStreamCols = 1024;
 template <typename T, int KM>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 2)
 reconstruct_stream_kernel(int64_t m, int64_t n, int k, const T* __restrict__ Af, int64_t ldaf,
                           const T* __restrict__ Bf, int64_t ldbf, const T* __restrict__ M, int64_t ldm,
                           T* __restrict__ L, int64_t ldl, T* __restrict__ S, int64_t lds, double* __restrict__ part,
-                          bool vec) {
-  constexpr int TR = 32, TC = 128, RPT = 4;
-  __shared__ T as[TR][KM + 1];
-  const int tid = threadIdx.x, tc = tid % 32, tr = tid / 32;
-  const int64_t r0 = (int64_t)blockIdx.y * TR, c0 = (int64_t)blockIdx.x * TC + 4 * tc;
-  for (int e = tid; e < TR * KM; e += 256) {
-    const int r = e / KM, t = e % KM;
-    as[r][t] = (r0 + r < m && t < k) ? Af[(r0 + r) * ldaf + t] : T(0);
+                          bool vec, int64_t rows_per_cta) {
+  constexpr int RPT = 4;
+  constexpr int KMP = (KM + 3) / 4 * 4;  // A rows padded to 16-byte multiples in shared memory
+  extern __shared__ __align__(16) unsigned char stream_smem[];
+  T* as = reinterpret_cast<T*>(stream_smem);  // [rows_per_cta][KMP], this CTA's rows of Af
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int64_t c0 = (int64_t)blockIdx.x * kStreamCols + 128 * warp + 4 * lane;
+  const int64_t rb = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t re = rb + rows_per_cta < m ? rb + rows_per_cta : m;
+  for (int64_t e = tid; e < (re - rb) * KMP; e += 256) {
+    const int64_t r = e / KMP;
+    const int t = (int)(e - r * KMP);
+    as[e] = t < k ? Af[(rb + r) * ldaf + t] : T(0);
   }
+  __syncthreads();
   T b[4][KM];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int t = 0; t < KM; ++t) b[q][t] = (c0 + q < n && t < k) ? Bf[(c0 + q) * ldbf + t] : T(0);
-  __syncthreads();
-  double r2 = 0.0, m2 = 0.0;
-  T mv[RPT][4];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {  // all loads first: 8 x 16 B in flight per thread
-    const int64_t r = r0 + tr * RPT + i;
-    if (r < m && M) {
-      if (vec && c0 + 3 < n) Vec4g<T>::ld(M + r * ldm + c0, mv[i]);
-      else
-#pragma unroll
-        for (int q = 0; q < 4; ++q) mv[i][q] = c0 + q < n ? M[r * ldm + c0 + q] : T(0);
-    }
+  const bool full = vec && c0 + 3 < n;
+  const bool any = c0 < n;
+#define L1F_LOAD_M(R0, DST)                                                                \
+  _Pragma("unroll") for (int i = 0; i < RPT; ++i) {                                        \
+    const int64_t r = (R0) + i;                                                            \
+    if (r < re && M && any) {                                                              \
+      if (full) Vec4g<T>::ld(M + r * ldm + c0, DST[i]);                                    \
+      else                                                                                 \
+        _Pragma("unroll") for (int q = 0; q < 4; ++q) DST[i][q] = c0 + q < n ? M[r * ldm + c0 + q] : T(0); \
+    } else {                                                                               \
+      _Pragma("unroll") for (int q = 0; q < 4; ++q) DST[i][q] = T(0);                     \
+    }                                                                                      \
   }
+  double m2 = 0.0;
+  T mv[RPT][4], mn[RPT][4];
+  L1F_LOAD_M(rb, mv)
+  for (int64_t r0 = rb; r0 < re; r0 += RPT) {
+    if (r0 + RPT < re) { L1F_LOAD_M(r0 + RPT, mn) }  // next rows in flight
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int ri = tr * RPT + i;
-    const int64_t r = r0 + ri;
-    if (r >= m) break;
-    T l[4] = {T(0), T(0), T(0), T(0)};
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = r0 + i;
+      if (r < re && any) {
+        T a[KMP];
 #pragma unroll
-    for (int t = 0; t < KM; ++t) {
-      const T a = as[ri][t];
+        for (int t = 0; t < KMP; t += 4) Vec4s<T>::ld(as + (r - rb) * KMP + t, a + t);  // broadcast
+        T l[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = fma(a, b[q][t], l[q]);
-    }
-    T sv[4];
+        for (int t = 0; t < KM; ++t)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      sv[q] = mv[i][q] - l[q];
-      const double d = (double)((mv[i][q] - l[q]) - sv[q]);
-      r2 += d * d;
-      m2 += (double)mv[i][q] * (double)mv[i][q];
-    }
-    if (vec && c0 + 3 < n) {
-      if (L) Vec4g<T>::st(L + r * ldl + c0, l);
-      if (M && S) Vec4g<T>::st(S + r * lds + c0, sv);
-    } else {
+          for (int q = 0; q < 4; ++q) l[q] = fma(a[t], b[q][t], l[q]);
+        T sv[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (c0 + q < n) {
-          if (L) L[r * ldl + c0 + q] = l[q];
-          if (M && S) S[r * lds + c0 + q] = sv[q];
+        for (int q = 0; q < 4; ++q) sv[q] = mv[i][q] - l[q];
+        if (full) {
+          if (L) Vec4g<T>::st(L + r * ldl + c0, l);
+          if (M && S) Vec4g<T>::st(S + r * lds + c0, sv);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q < n) {
+              if (L) L[r * ldl + c0 + q] = l[q];
+              if (M && S) S[r * lds + c0 + q] = sv[q];
+            }
         }
+      }
     }
+    {  // sum(M^2): this step's 16 products in T, folded into the double once per step
+      T acc = T(0);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = fma(mv[i][q], mv[i][q], acc);
+      m2 += (double)acc;
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) mv[i][q] = mn[i][q];
   }
+#undef L1F_LOAD_M
   if (part) {
     const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    double r2 = 0.0;
     block_sum2(r2, m2, &part[2 * blk], &part[2 * blk + 1]);
   }
 }
@@ -530,7 +572,17 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
     if (rc != L1F_ERR_UNSUPPORTED) return rc;
   }
   const bool small = k <= 16;
-  dim3 grid = small ? dim3((unsigned)ceil_div(n, 128), (unsigned)ceil_div(m, 32))
+  // streaming kernel: 1024-column strips x row ranges, ~4 CTAs per SM in total (2 resident) so
+  // each CTA streams many rows with its Bf columns in registers
+  const int64_t strips = ceil_div(n, kStreamCols);
+  const int64_t want_ctas = (int64_t)num_sms() * 4;
+  const size_t esz_s = dtype == L1F_F32 ? 4 : 8;
+  const int64_t max_rows = (int64_t)(48 * 1024 / (esz_s * 16)) / 4 * 4;  // Af rows held in shared memory
+  int64_t row_groups = std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 4), ceil_div(want_ctas, strips)));
+  int64_t rows_per_cta = ceil_div(ceil_div(m, row_groups), 4) * 4;
+  if (rows_per_cta > max_rows) rows_per_cta = max_rows;
+  row_groups = ceil_div(m, rows_per_cta);
+  dim3 grid = small ? dim3((unsigned)strips, (unsigned)row_groups)
                     : dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(m, kTile));
   L1F_REQUIRE(grid.y <= 65535, L1F_ERR_UNSUPPORTED, "reconstruct: too many row tiles");
   const int64_t nblk = (int64_t)grid.x * grid.y;
@@ -543,8 +595,10 @@ extern "C" int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k, const
   const bool vec = (!M || (al16(M) && (ldm * esz) % 16 == 0)) && (!L || (al16(L) && (ldl * esz) % 16 == 0)) &&
                    (!S || (al16(S) && (lds * esz) % 16 == 0));
 #define L1F_STREAM(TT, KM)                                                                                       \
-  reconstruct_stream_kernel<TT, KM><<<grid, 256, 0, st>>>(m, n, k, (const TT*)Af, ldaf, (const TT*)Bf, ldbf,   \
-                                                         (const TT*)M, ldm, (TT*)L, ldl, (TT*)S, lds, pp, vec)
+  reconstruct_stream_kernel<TT, KM><<<grid, 256, (size_t)rows_per_cta * ((KM + 3) / 4 * 4) * sizeof(TT), st>>>( \
+      m, n, k, (const TT*)Af, ldaf, (const TT*)Bf, ldbf,                                                          \
+                                                         (const TT*)M, ldm, (TT*)L, ldl, (TT*)S, lds, pp, vec,    \
+                                                         rows_per_cta)
   if (small) {
     if (dtype == L1F_F32) {
       switch ((k + 1) / 2) {
