@@ -48,7 +48,7 @@ constexpr int TSP = TS;       // fp32 rows of the partial-z inbox
 constexpr int RING = 4;
 constexpr int kStallIters = 20;      // STAGNATION_ITERS, l1reg.py:34
 constexpr float kStallEps = 1e-12f;  // STAGNATION_EPS, l1reg.py:33
-constexpr uint32_t TMEM_COLS = 128;  // per group: phase a 32 columns, then 32 per phase-c M tile
+constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, then 96 per phase-c M tile
 
 struct Params {
   int s, k, cluster, rs;
@@ -191,9 +191,6 @@ __device__ __forceinline__ void st_async16u(uint32_t peer_dst, uint4 v, uint32_t
                ::"r"(peer_dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(peer_bar) : "memory");
 }
 
-// products (i, j) of the 3-piece split kept: i + j <= 2
-__host__ __device__ constexpr int term_a(int t) { return t == 2 || t == 4 ? 1 : t == 5 ? 2 : 0; }
-__host__ __device__ constexpr int term_b(int t) { return t == 1 || t == 4 ? 1 : t == 3 ? 2 : 0; }
 
 // per-slot max|r| of N slots over the warp's 32 rows: reduce-scatter butterfly; afterwards lane l
 // holds slot l / (32 / N) (reduced over all 32 lanes)
@@ -226,10 +223,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr int WPG = GT / 32;             // warps per group (4 per TMEM lane quarter at NG = 1)
   constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (16 at NG = 2, 8 at NG = 1)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
-  constexpr int NTERM = NA == 3 ? 6 : 5;   // products (i, j), i + j <= 2, i < NA
-  constexpr uint32_t GCOLS = 32u * (1 + MTC);
+  constexpr uint32_t GCOLS = 96u * (1 + MTC);
   static_assert(NG * GCOLS <= TMEM_COLS, "TMEM columns");
-  constexpr size_t A_PIECE = (size_t)SL * KP, Z_PIECE = (size_t)KP * TS, V_PIECE = (size_t)SL * TS;
+  constexpr size_t A_PIECE = (size_t)SL * KP, Z_PIECE = (size_t)KP * TS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Group groups[NG];
   __shared__ uint32_t tmem_base;
@@ -394,8 +390,13 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   // A MN-major for phase c (SBO: next 8 columns = M, LBO: next 8 rows = K); z and v MN-major
   // (SBO: next 8 slots, LBO: next 8 rows of K).
   const uint32_t a_addr = umma::saddr(aop), z_addr = umma::saddr(zop), v_addr = umma::saddr(vop);
-  constexpr uint32_t ID_A = idesc_bf16(128, TS, 0, 1);
-  constexpr uint32_t ID_C = idesc_bf16(128, TS, 1, 1);
+  // z and v operands hold their three pieces side by side along N (n = 32 p + slot), so one MMA
+  // per dictionary piece and K step: a0 [z0 z1 z2] -> columns 0-95, a1 [z0 z1] -> 32-95,
+  // a2 [z0] -> 64-95; column block j then holds the products of order j (i + j' = j)
+  constexpr uint32_t ID_A96 = idesc_bf16(128, 96, 0, 1), ID_A64 = idesc_bf16(128, 64, 0, 1),
+                     ID_A32 = idesc_bf16(128, 32, 0, 1);
+  constexpr uint32_t ID_C96 = idesc_bf16(128, 96, 1, 1), ID_C64 = idesc_bf16(128, 64, 1, 1),
+                     ID_C32 = idesc_bf16(128, 32, 1, 1);
   const uint32_t bar_p = umma::saddr(&G.bar_p), bar_r = umma::saddr(&G.bar_r);
 
   uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
@@ -409,13 +410,12 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       umma::fence_after();
 #pragma unroll 1
       for (int ks = 0; ks < KP / 16; ++ks) {
-#pragma unroll
-        for (int tt = 0; tt < NTERM; ++tt) {
-          const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * A_PIECE * 2) + (uint32_t)(2 * ks) * 128u;
-          const uint32_t bb = z_addr + (uint32_t)(term_b(tt) * Z_PIECE * 2) + (uint32_t)(2 * ks) * 512u;
-          mma_bf16(tmem, umma::desc_noswz(aa, 128, KG * 128), umma::desc_noswz(bb, 512, 128), ID_A,
-                   (ks | tt) != 0);
-        }
+        const uint64_t db = umma::desc_noswz(z_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
+        const uint32_t aa = a_addr + (uint32_t)(2 * ks) * 128u;
+        mma_bf16(tmem, umma::desc_noswz(aa, 128, KG * 128), db, ID_A96, ks != 0);
+        mma_bf16(tmem + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), 128, KG * 128), db, ID_A64, 1u);
+        if (NA == 3)
+          mma_bf16(tmem + 64, umma::desc_noswz(aa + (uint32_t)(2 * A_PIECE * 2), 128, KG * 128), db, ID_A32, 1u);
       }
       umma::commit(&G.bar_a);
     }
@@ -425,9 +425,15 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     umma::fence_after();
     stamp(1);
     float az[SPT];
-    if constexpr (SPT == 16) umma::ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0, az);
-    else umma::ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0, az);
-    umma::ld_wait();
+    {  // the three order blocks, summed smallest first
+      float b0[SPT], b1[SPT], b2[SPT];
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0;
+      if constexpr (SPT == 16) { umma::ld16(ta, b0); umma::ld16(ta + 32, b1); umma::ld16(ta + 64, b2); }
+      else { umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2); }
+      umma::ld_wait();
+#pragma unroll
+      for (int j = 0; j < SPT; ++j) az[j] = (b2[j] + b1[j]) + b0[j];
+    }
     {
       const uint32_t fm = (G.fmask >> slot0) & ((1u << SPT) - 1u);
       if (fm) {
@@ -461,14 +467,14 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       az[j] = sup ? azv + sgt : x + yb;     // v = (x - e) + y / b
       yr[j] = y;
     }
-    // v operand: MN-major core matrices (row group rg, slot group sg) at (rg * 4 + sg) * 64
+    // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
 #pragma unroll
     for (int hh = 0; hh < SPT / 8; ++hh) {
       float v8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
-      const size_t off = (size_t)((lrow >> 3) * 4 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
-      split8_store(v8, vop + off, vop + V_PIECE + off, vop + 2 * V_PIECE + off);
+      const size_t off = (size_t)((lrow >> 3) * 12 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
+      split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
     }
     {  // per-slot max|r| over this warp's 32 rows
       const float m = slot_max<SPT>(rmax, lane);
@@ -484,16 +490,15 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       umma::fence_after();
 #pragma unroll
       for (int mt = 0; mt < MTC; ++mt) {
+        const uint32_t dc = tmem + 96u * (1 + mt);
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
-#pragma unroll
-          for (int tt = 0; tt < NTERM; ++tt) {
-            const uint32_t aa = a_addr + (uint32_t)(term_a(tt) * A_PIECE * 2) + (uint32_t)(2 * ks) * (KG * 128u) +
-                                (uint32_t)(16 * mt) * 128u;
-            const uint32_t bb = v_addr + (uint32_t)(term_b(tt) * V_PIECE * 2) + (uint32_t)(2 * ks) * 512u;
-            mma_bf16(tmem + 32u * (1 + mt), umma::desc_noswz(aa, KG * 128, 128), umma::desc_noswz(bb, 512, 128), ID_C,
-                     (ks | tt) != 0);
-          }
+          const uint64_t db = umma::desc_noswz(v_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
+          const uint32_t aa = a_addr + (uint32_t)(2 * ks) * (KG * 128u) + (uint32_t)(16 * mt) * 128u;
+          mma_bf16(dc, umma::desc_noswz(aa, KG * 128, 128), db, ID_C96, ks != 0);
+          mma_bf16(dc + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), db, ID_C64, 1u);
+          if (NA == 3)
+            mma_bf16(dc + 64, umma::desc_noswz(aa + (uint32_t)(2 * A_PIECE * 2), KG * 128, 128), db, ID_C32, 1u);
         }
       }
       umma::commit(&G.bar_c);
@@ -527,9 +532,15 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 #pragma unroll
     for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
       float zp[SPT];
-      if constexpr (SPT == 16) umma::ld16(tmem + ((uint32_t)(32 * q) << 16) + 32u * (1 + mt) + (uint32_t)slot0, zp);
-      else umma::ld8(tmem + ((uint32_t)(32 * q) << 16) + 32u * (1 + mt) + (uint32_t)slot0, zp);
-      umma::ld_wait();
+      {
+        float b0[SPT], b1[SPT], b2[SPT];
+        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * (1 + mt) + (uint32_t)slot0;
+        if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
+        else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
+        umma::ld_wait();
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
+      }
       const int t = 128 * mt + lrow;
       if (t < KP) {
         const int owner = t / rs, row = t - owner * rs;
@@ -647,18 +658,18 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         stamp(7);
         uint4 w0, w1, w2;
         split8(v8, w0, w1, w2);
-        const size_t off = (size_t)((t >> 3) * 4 + sg) * 64 + (t & 7) * 8;
+        const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
         stamp(8);
         if (rep == 0) {
           float* dz = zs_cur + (size_t)row * TS + 8 * sg;
           *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
           *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
           *reinterpret_cast<uint4*>(zop + off) = w0;
-          *reinterpret_cast<uint4*>(zop + Z_PIECE + off) = w1;
-          *reinterpret_cast<uint4*>(zop + 2 * Z_PIECE + off) = w2;
+          *reinterpret_cast<uint4*>(zop + 4 * 64 + off) = w1;
+          *reinterpret_cast<uint4*>(zop + 8 * 64 + off) = w2;
         }
-        const uint32_t a0 = umma::saddr(zop + off), a1 = umma::saddr(zop + Z_PIECE + off),
-                       a2 = umma::saddr(zop + 2 * Z_PIECE + off);
+        const uint32_t a0 = umma::saddr(zop + off), a1 = umma::saddr(zop + 4 * 64 + off),
+                       a2 = umma::saddr(zop + 8 * 64 + off);
         for (int d = rep; d < C - 1; d += nrep) {
           const int peer = d < crank ? d : d + 1;
           const uint32_t pb = peer_addr(bar_r, peer);

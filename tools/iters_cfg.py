@@ -18,3 +18,10 @@ print(f"[{tag}] sigma range {sig.min():.3g}..{sig.max():.3g}")
 for side in ("c", "r"):
     it = f["iters_" + side].cpu().numpy(); st = f["status_" + side].cpu().numpy()
     print(f"[{tag}] {side}: mean {it.mean():.2f} max {it.max()} status {np.bincount(st, minlength=4)} p50 {np.median(it)}")
+for side, x in (("c", None), ("r", None)):
+    st = f["status_" + side].cpu().numpy()
+    bad = np.flatnonzero((st == 1) | (st == 2))
+    if bad.size:
+        res = f["res_" + side].cpu().numpy()
+        it = f["iters_" + side].cpu().numpy()
+        print(f"[{tag}] {side}: failed units {bad[:10]} status {st[bad[:10]]} iters {it[bad[:10]]} res {res[bad[:10]]}")
