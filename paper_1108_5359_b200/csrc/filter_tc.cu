@@ -544,16 +544,21 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       const int t = 128 * mt + lrow;
       if (t < KP) {
         const int owner = t / rs, row = t - owner * rs;
-        float* dst = zin + (size_t)(crank * rs + row) * TSP + slot0;
+        // inbox row zr of the owner; its 16-byte chunks are XOR-swizzled by (zr & 7) so that the
+        // owner's (row, slot-group) sum reads are bank-conflict free
+        const int zr = crank * rs + row;
+        float* drow = zin + (size_t)zr * TSP;
         if (owner == crank) {
 #pragma unroll
           for (int i = 0; i < SPT / 4; ++i)
-            *reinterpret_cast<float4*>(dst + 4 * i) = make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
+            *reinterpret_cast<float4*>(drow + 4 * ((slot0 / 4 + i) ^ (zr & 7))) =
+                make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
         } else {
-          const uint32_t pdst = peer_addr(umma::saddr(dst), owner), pbar = peer_addr(bar_p, owner);
+          const uint32_t prow = peer_addr(umma::saddr(drow), owner), pbar = peer_addr(bar_p, owner);
 #pragma unroll
           for (int i = 0; i < SPT / 4; ++i)
-            st_async16v(pdst + 16 * i, zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3], pbar);
+            st_async16v(prow + 16 * ((slot0 / 4 + i) ^ (zr & 7)), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3],
+                        pbar);
         }
       }
     }
@@ -626,21 +631,22 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       const int nitems = vmine * 4;
       const int nrep = nitems > 0 ? max(1, (GT - 32) / nitems) : 1;
       const int item = gt2 % max(nitems, 1), rep = gt2 / max(nitems, 1);
+      const bool active = true;
       if (nitems > 0 && rep < nrep) {
         const int row = item >> 2, sg = item & 3, t = r0 + row;
         float v8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = 0.f;
         {  // fixed summation order c = 0 .. C-1 (results independent of the unrolling)
-          const float* src0 = zin + (size_t)row * TSP + 8 * sg;
-          const size_t cstride = (size_t)rs * TSP;
           int c = 0;
           for (; c + 4 <= C; c += 4) {
             float4 a[4], b[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              a[u] = *reinterpret_cast<const float4*>(src0 + (c + u) * cstride);
-              b[u] = *reinterpret_cast<const float4*>(src0 + (c + u) * cstride + 4);
+              const int zr = (c + u) * rs + row;
+              const float* src = zin + (size_t)zr * TSP;
+              a[u] = *reinterpret_cast<const float4*>(src + 4 * ((2 * sg) ^ (zr & 7)));
+              b[u] = *reinterpret_cast<const float4*>(src + 4 * ((2 * sg + 1) ^ (zr & 7)));
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -649,8 +655,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
             }
           }
           for (; c < C; ++c) {
-            const float4 a = *reinterpret_cast<const float4*>(src0 + c * cstride);
-            const float4 b = *reinterpret_cast<const float4*>(src0 + c * cstride + 4);
+            const int zr = c * rs + row;
+            const float* src = zin + (size_t)zr * TSP;
+            const float4 a = *reinterpret_cast<const float4*>(src + 4 * ((2 * sg) ^ (zr & 7)));
+            const float4 b = *reinterpret_cast<const float4*>(src + 4 * ((2 * sg + 1) ^ (zr & 7)));
             v8[0] += a.x; v8[1] += a.y; v8[2] += a.z; v8[3] += a.w;
             v8[4] += b.x; v8[5] += b.y; v8[6] += b.z; v8[7] += b.w;
           }
@@ -660,7 +668,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         split8(v8, w0, w1, w2);
         const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
         stamp(8);
-        if (rep == 0) {
+        if (active && rep == 0) {
           float* dz = zs_cur + (size_t)row * TS + 8 * sg;
           *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
           *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
@@ -670,7 +678,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         }
         const uint32_t a0 = umma::saddr(zop + off), a1 = umma::saddr(zop + 4 * 64 + off),
                        a2 = umma::saddr(zop + 8 * 64 + off);
-        for (int d = rep; d < C - 1; d += nrep) {
+        for (int d = rep; active && d < C - 1; d += nrep) {
           const int peer = d < crank ? d : d + 1;
           const uint32_t pb = peer_addr(bar_r, peer);
           st_async16u(peer_addr(a0, peer), w0, pb);
