@@ -6,11 +6,12 @@
 // (exact in TF32) and lo = x - hi, and L = Ah Bh^T + Ah Bl^T + Al Bh^T accumulated in FP32 in
 // TMEM (error ~2^-22 relative per product; the parity gate is 1e-4).
 //
-// Persistent CTAs (one per SM), 12 warps:
+// Persistent CTAs (one per SM), 16 warps:
 //   warp 0      TMA producer: fp32 chunks of Af (128 x 32) and Bf (128 x 32), SWIZZLE_128B, K-major
 //   warp 1      TMEM allocation + MMA issuer (one thread): 12 tcgen05.mma.kind::tf32 per chunk
-//   warps 4-7   splitters: hi in place, lo into a second buffer (same swizzled layout)
-//   warps 8-11  epilogue: tcgen05.ld (row per thread), M via TMA (double buffered), S = M - L,
+//   warps 4-7   splitters: lo = x - hi into a second buffer (same swizzled layout); hi is the fp32
+//               word itself (kind::tf32 ignores its low 13 mantissa bits)
+//   warps 8-15  epilogue: tcgen05.ld (row x 16 columns per thread), M via TMA, S = M - L,
 //               L and S staged in shared memory and written with TMA stores
 // Two 128x128 FP32 accumulators in TMEM (256 columns) overlap the MMA of tile t+1 with the
 // epilogue of tile t; two smem stages overlap loads, splits and MMAs.  Edges are handled by TMA
@@ -27,9 +28,17 @@ namespace l1f {
 namespace rtc {
 
 constexpr int BM = 128, BN = 128, BK = 16;      // K chunk of 16 fp32 = 64-byte rows (SWIZZLE_64B)
-constexpr int STAGES = 3;
-constexpr int NMB = 6;                          // M buffers (prefetch distance 4 chunks)
-constexpr int NTHREADS = 384;
+#ifndef L1F_RTC_STAGES
+#define L1F_RTC_STAGES 4
+#endif
+#ifndef L1F_RTC_NMB
+#define L1F_RTC_NMB 4
+#endif
+constexpr int STAGES = L1F_RTC_STAGES;          // operand stages (TMA -> lo split -> MMA)
+constexpr int NMB = L1F_RTC_NMB;                // M buffers
+constexpr int MPF = NMB - 2;                    // M prefetch distance (chunks)
+constexpr int NTHREADS = 512;
+constexpr int EPI = 256;  // epilogue threads: warps 8-15, two per TMEM lane quarter (16 columns each)
 constexpr uint32_t OP_BYTES = BM * BK * 4;      // 8 KB: one 128 x 16 fp32 operand box
 constexpr uint32_t CHUNK_BYTES = BM * 32 * 4;   // 16 KB: one 128 x 32 fp32 epilogue box (SWIZZLE_128B)
 constexpr int GROUP = 8;                        // row tiles per raster group (L2 reuse of Bf)
@@ -46,7 +55,7 @@ struct Smem {
   unsigned long long tfull[2], tempty[2];
   unsigned long long mfull[NMB];
   uint32_t tmem_base;
-  double red[2][4];
+  double red[2][8];
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -126,7 +135,7 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.conv[s], 1); mbar_init(&sm.empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], EPI); }
     for (int b = 0; b < NMB; ++b) mbar_init(&sm.mfull[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -204,7 +213,8 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
             lo[e] = make_float4(__uint_as_float(x.x) - __uint_as_float(h.x), __uint_as_float(x.y) - __uint_as_float(h.y),
                                 __uint_as_float(x.z) - __uint_as_float(h.z), __uint_as_float(x.w) - __uint_as_float(h.w));
-            raw[e] = h;
+            // hi stays in place: the tensor core reads TF32 from the fp32 word and ignores the low
+            // 13 mantissa bits, i.e. uses exactly h
           }
         }
         fence_async_smem();
@@ -214,7 +224,8 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   } else if (warp >= 8) {
     // ================= epilogue (128 threads, TMEM lane quarter = warp - 8)
-    const int q = warp - 8, row = 32 * q + lane;  // row of the tile owned by this thread
+    const int ew = warp - 8, q = ew & 3, half = ew >> 2;
+    const int row = 32 * q + lane;  // row of the tile owned by this thread (columns half * 16 .. + 16)
     const bool leader = threadIdx.x == 256;
     double r2 = 0.0, m2 = 0.0;
     int ti = 0, g = 0;
@@ -230,7 +241,7 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       return true;
     };
     if (leader && has_m) {  // M of the first four chunks
-      for (int gg = 0; gg < 4; ++gg) {
+      for (int gg = 0; gg < MPF; ++gg) {
         int x, y;
         if (chunk_coords(gg, x, y)) {
           mbar_expect_arrive(&sm.mfull[gg], CHUNK_BYTES);
@@ -246,15 +257,12 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       asm volatile("tcgen05.fence::after_thread_sync;");
       for (int cc = 0; cc < BN / 32; ++cc, ++g) {
         const int mb = g % NMB, lb = g & 1;
-        uint32_t v[32];
-        const uint32_t taddr = tmem + (uint32_t)(acc * BN + cc * 32) + ((uint32_t)(32 * q) << 16);
+        uint32_t v[16];
+        const uint32_t taddr = tmem + (uint32_t)(acc * BN + cc * 32 + 16 * half) + ((uint32_t)(32 * q) << 16);
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (cc == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
@@ -262,44 +270,40 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           mbar_arrive(&sm.tempty[acc]);
         }
         if (leader) {
-          // stores of chunk g-2 (lbuf[lb], mbuf[(g-2) % NMB]) have finished reading shared memory
+          // stores of chunk g-2 (lbuf[lb], its M buffer) have finished reading shared memory
           tma_wait_read1();
-          if (has_m) {  // prefetch M of chunk g+4 into the buffer freed above
+          if (has_m) {  // prefetch M of chunk g+MPF into the buffer freed above
             int x, y;
-            if (chunk_coords(g + 4, x, y)) {
-              const int nb = (g + 4) % NMB;
+            if (chunk_coords(g + MPF, x, y)) {
+              const int nb = (g + MPF) % NMB;
               mbar_expect_arrive(&sm.mfull[nb], CHUNK_BYTES);
               tma_load(sm.mbuf[nb], &tmM, x, y, &sm.mfull[nb]);
             }
           }
         }
         if (has_m) mbar_wait(&sm.mfull[mb], (g / NMB) & 1);
-        named_bar(1, 128);
+        named_bar(1, EPI);
         // 16-byte chunk j of this row sits at position j ^ (row & 7) (SWIZZLE_128B)
         float4* mrow = reinterpret_cast<float4*>(sm.mbuf[mb] + row * 128);
         float4* lrow = reinterpret_cast<float4*>(sm.lbuf[lb] + row * 128);
+        // sum(M^2) of this row's 32 entries in FP32, folded into the double once per chunk; the
+        // residual partial of (M - L) - S is identically 0 (S is stored as the fp32 M - L)
+        float macc = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int p = j ^ (row & 7);
-          const float4 l4 = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                        __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = 4 * half + jj, p = j ^ (row & 7);
+          const float4 l4 = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
+                                        __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
           if (has_l) lrow[p] = l4;
           if (has_m) {
             const float4 m4 = mrow[p];
-            const float4 s4 = make_float4(m4.x - l4.x, m4.y - l4.y, m4.z - l4.z, m4.w - l4.w);
-            mrow[p] = s4;  // S in place of M (each thread owns its row)
-            const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w},
-                        ss[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const double dd = (double)((mm[u] - ll[u]) - ss[u]);
-              r2 += dd * dd;
-              m2 += (double)mm[u] * (double)mm[u];
-            }
+            mrow[p] = make_float4(m4.x - l4.x, m4.y - l4.y, m4.z - l4.z, m4.w - l4.w);  // S in place of M
+            macc = fmaf(m4.x, m4.x, fmaf(m4.y, m4.y, fmaf(m4.z, m4.z, fmaf(m4.w, m4.w, macc))));
           }
         }
+        m2 += (double)macc;
         fence_async_smem();
-        named_bar(1, 128);
+        named_bar(1, EPI);
         if (leader) {
           const int x = tn * BN + cc * 32, y = tm * BM;
           if (has_l) tma_store(&tmL, x, y, sm.lbuf[lb]);
@@ -312,11 +316,11 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // per-CTA residual partials (deterministic)
     r2 = warp_sum(r2);
     m2 = warp_sum(m2);
-    if (lane == 0) { sm.red[0][q] = r2; sm.red[1][q] = m2; }
-    named_bar(1, 128);
+    if (lane == 0) { sm.red[0][ew] = r2; sm.red[1][ew] = m2; }
+    named_bar(1, EPI);
     if (leader && part) {
       double a = 0, c = 0;
-      for (int i = 0; i < 4; ++i) { a += sm.red[0][i]; c += sm.red[1][i]; }
+      for (int i = 0; i < 8; ++i) { a += sm.red[0][i]; c += sm.red[1][i]; }
       part[2 * blockIdx.x] = a;
       part[2 * blockIdx.x + 1] = c;
     }
