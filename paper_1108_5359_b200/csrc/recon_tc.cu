@@ -14,7 +14,7 @@
 //   warps 8-15  epilogue: tcgen05.ld (row x 16 columns per thread), M via TMA, S = M - L,
 //               L and S staged in shared memory and written with TMA stores
 // Two 128x128 FP32 accumulators in TMEM (256 columns) overlap the MMA of tile t+1 with the
-// epilogue of tile t; two smem stages overlap loads, splits and MMAs.  Edges are handled by TMA
+// epilogue of tile t; four operand stages overlap loads, splits and MMAs.  Edges are handled by TMA
 // (zero fill on load, clipping on store).  12 B of DRAM traffic per output entry.
 #include "common.cuh"
 
