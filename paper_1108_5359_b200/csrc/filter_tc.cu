@@ -73,6 +73,7 @@ struct Group {
   long long head, tail, pf_from, pf_to;
   alignas(8) unsigned long long bar_p, bar_r, bar_a, bar_c;
   uint32_t fmask;
+  uint32_t zmask[2];  // TA: by pass parity, slots whose z_it is 0 (fresh or empty)
 };
 
 template <int KP, int NA>
@@ -143,6 +144,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
+// A operand from TMEM (K-major: lane = row of A, 8 columns per K = 16 step)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d, uint32_t ta, uint64_t db, uint32_t id, uint32_t acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }"
+               ::"r"(d), "r"(ta), "l"(db), "r"(id), "r"(acc) : "memory");
+}
 __device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
   asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
                ::"r"(d), "l"(da), "l"(db), "r"(id), "r"(acc) : "memory");
@@ -212,8 +218,13 @@ __device__ __forceinline__ float slot_max(float (&v)[N], int lane) {
   return v[0];
 }
 
-// KP: padded k (multiple of 16); NG: slot groups per CTA; NA: bf16 pieces of the dictionary
-template <int KP, int NG, int NA>
+// KP: padded k (multiple of 16); NG: slot groups per CTA; NA: bf16 pieces of the shared-memory
+// dictionary.  TA (large k, one group): phase a reads a 3-piece copy of the dictionary from TMEM
+// (K-major, lane = row, two bf16 per column), phase c the NA = 2-piece copy in shared memory, and
+// z is updated in residual form, z_{it+1} = z_it + A^T (v - A z_it): identical to the reference's
+// z = A^T v for orthonormal A, and its fixed point does not depend on the precision of phase c
+// (only phase a defines the model A z whose residual is tested).
+template <int KP, int NG, int NA, bool TA>
 __global__ void __launch_bounds__(NT, 1)
 adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t lda, const float* __restrict__ scale,
               Params P, Layout Lo, float* __restrict__ Z, float* __restrict__ E, int32_t* __restrict__ iters,
@@ -223,8 +234,12 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr int WPG = GT / 32;             // warps per group (4 per TMEM lane quarter at NG = 1)
   constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (16 at NG = 2, 8 at NG = 1)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
-  constexpr uint32_t GCOLS = 96u * (1 + MTC);
-  static_assert(NG * GCOLS <= TMEM_COLS, "TMEM columns");
+  constexpr uint32_t ACOLS = TA ? (3u * KP / 2 + 31u) / 32u * 32u : 0u;  // TMEM columns of the TA dictionary
+  constexpr uint32_t GCOLS = TA ? 96u + 32u * MTC : 96u * (1 + MTC);
+  static_assert(!TA || NG == 1, "TA runs one slot group");
+  static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
+  static_assert(ACOLS + NG * GCOLS <= TMEM_COLS, "TMEM columns");
+
   constexpr size_t A_PIECE = (size_t)SL * KP, Z_PIECE = (size_t)KP * TS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Group groups[NG];
@@ -273,6 +288,35 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  if constexpr (TA) {  // 3-piece dictionary rows into TMEM: lane = row, column c = pieces of k 2c, 2c+1
+    const int q4 = warp & 3, part = warp >> 2;  // 4 warps per lane quarter split the column range
+    const int r = 32 * q4 + lane, row = row_base + r;
+    const float* arow = A + (int64_t)(row < P.s ? row : 0) * lda;
+    constexpr int CP = KP / 2;  // columns per piece
+    for (int c0 = 8 * part; c0 < CP; c0 += 32) {
+      uint32_t w[3][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = 2 * (c0 + u);
+        const float x0 = (row < P.s && t < P.k) ? arow[t] : 0.f, x1 = (row < P.s && t + 1 < P.k) ? arow[t + 1] : 0.f;
+        w[0][u] = cvt_bf16x2(x0, x1);
+        const float r0 = x0 - bf_lo(w[0][u]), r1 = x1 - bf_hi(w[0][u]);
+        w[1][u] = cvt_bf16x2(r0, r1);
+        w[2][u] = cvt_bf16x2(r0 - bf_lo(w[1][u]), r1 - bf_hi(w[1][u]));
+      }
+#pragma unroll
+      for (int pc = 0; pc < 3; ++pc)
+        if (c0 < CP)
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                       ::"r"(tmem_base + (uint32_t)(pc * CP + c0) + ((uint32_t)(32 * q4) << 16)), "r"(w[pc][0]),
+                       "r"(w[pc][1]), "r"(w[pc][2]), "r"(w[pc][3]), "r"(w[pc][4]), "r"(w[pc][5]), "r"(w[pc][6]),
+                       "r"(w[pc][7]) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
   if (C > 1) cluster.sync();  // peers' mbarriers initialised before any DSMEM traffic
 
   // ================================================================ one slot group
@@ -287,7 +331,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RING][SL]
   float* rall = reinterpret_cast<float*>(gb + Lo.rall);    // [2][C][TS] per-CTA slot max|r| (parity)
   float* rpart = reinterpret_cast<float*>(gb + Lo.rpart);  // [4][TS]
-  const uint32_t tmem = tmem_base + GCOLS * g;
+  const uint32_t tmem = tmem_base + ACOLS + GCOLS * g;
   const int vid = cid * NG + g, nv = nclusters * NG;      // units vid, vid + nv, ...
 
   // phase b mapping: TMEM lane quarter q (rows 32q .. 32q+31), slots [SPT h, SPT h + SPT)
@@ -374,6 +418,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     G.tail = RING;
     for (int sl = 0; sl < TS; ++sl) claim_into(sl);
     G.fmask = 0;
+    G.zmask[0] = 0xFFFFFFFFu;
     G.pf_from = G.tail;
     G.pf_to = G.head + RING;
     if (G.pf_to < G.pf_from) G.pf_to = G.pf_from;
@@ -411,11 +456,18 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 #pragma unroll 1
       for (int ks = 0; ks < KP / 16; ++ks) {
         const uint64_t db = umma::desc_noswz(z_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
-        const uint32_t aa = a_addr + (uint32_t)(2 * ks) * 128u;
-        mma_bf16(tmem, umma::desc_noswz(aa, 128, KG * 128), db, ID_A96, ks != 0);
-        mma_bf16(tmem + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), 128, KG * 128), db, ID_A64, 1u);
-        if (NA == 3)
-          mma_bf16(tmem + 64, umma::desc_noswz(aa + (uint32_t)(2 * A_PIECE * 2), 128, KG * 128), db, ID_A32, 1u);
+        if constexpr (TA) {  // dictionary pieces from TMEM
+          const uint32_t ta = tmem_base + (uint32_t)(8 * ks);
+          mma_bf16_ts(tmem, ta, db, ID_A96, ks != 0);
+          mma_bf16_ts(tmem + 32, ta + (uint32_t)(KP / 2), db, ID_A64, 1u);
+          mma_bf16_ts(tmem + 64, ta + (uint32_t)KP, db, ID_A32, 1u);
+        } else {
+          const uint32_t aa = a_addr + (uint32_t)(2 * ks) * 128u;
+          mma_bf16(tmem, umma::desc_noswz(aa, 128, KG * 128), db, ID_A96, ks != 0);
+          mma_bf16(tmem + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), 128, KG * 128), db, ID_A64, 1u);
+          if (NA == 3)
+            mma_bf16(tmem + 64, umma::desc_noswz(aa + (uint32_t)(2 * A_PIECE * 2), 128, KG * 128), db, ID_A32, 1u);
+        }
       }
       umma::commit(&G.bar_a);
     }
@@ -464,7 +516,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       const bool sup = fabsf(w) > tn;
       const float sgt = w > 0.f ? tn : -tn;
       lr[j] = sup ? (azv - yb) + sgt : x;
-      az[j] = sup ? azv + sgt : x + yb;     // v = (x - e) + y / b
+      if constexpr (TA) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
+      else az[j] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
       yr[j] = y;
     }
     // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
@@ -489,7 +542,21 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll
-      for (int mt = 0; mt < MTC; ++mt) {
+      for (int mt = 0; mt < MTC && TA; ++mt) {  // 3 products (a0 v0, a0 v1, a1 v0) of 2-piece A and v'
+        const uint32_t dc = tmem + 96u + 32u * mt;
+#pragma unroll 1
+        for (int ks = 0; ks < SL / 16; ++ks) {
+          const uint32_t aa = a_addr + (uint32_t)(2 * ks) * (KG * 128u) + (uint32_t)(16 * mt) * 128u;
+          const uint32_t vb = v_addr + (uint32_t)(2 * ks) * 1536u;
+          const uint64_t da0 = umma::desc_noswz(aa, KG * 128, 128);
+          mma_bf16(dc, da0, umma::desc_noswz(vb, 1536, 128), ID_C32, ks != 0);
+          mma_bf16(dc, da0, umma::desc_noswz(vb + 4u * 128u, 1536, 128), ID_C32, 1u);
+          mma_bf16(dc, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), umma::desc_noswz(vb, 1536, 128),
+                   ID_C32, 1u);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MTC && !TA; ++mt) {
         const uint32_t dc = tmem + 96u * (1 + mt);
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
@@ -532,7 +599,12 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 #pragma unroll
     for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
       float zp[SPT];
-      {
+      if constexpr (TA) {
+        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u + 32u * mt + (uint32_t)slot0;
+        if constexpr (SPT == 16) umma::ld16(tc, zp);
+        else umma::ld8(tc, zp);
+        umma::ld_wait();
+      } else {
         float b0[SPT], b1[SPT], b2[SPT];
         const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * (1 + mt) + (uint32_t)slot0;
         if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
@@ -623,20 +695,31 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       }
       __syncwarp();
       publish(lane);
+      if constexpr (TA) {
+        const unsigned zm = __ballot_sync(0xffffffffu, !(G.state[lane] == 1) || G.it[lane] == 0);
+        if (lane == 0) G.zmask[par ^ 1] = zm;
+      }
     } else {
       // ========== round 2: sum my slice, split into bf16 pieces, push the pieces to every CTA.
       // Item (row, 8-slot group) is handled by nrep threads; each sums it (cheap, redundant) and
       // pushes the pieces from registers to every nrep-th peer; replica 0 also stores locally.
       const int gt2 = gtid - 32;
       const int nitems = vmine * 4;
-      const int nrep = nitems > 0 ? max(1, (GT - 32) / nitems) : 1;
+      const int nrep = nitems > 0 ? min(4, max(1, (GT - 32) / nitems)) : 1;  // each re-reads all C partials
       const int item = gt2 % max(nitems, 1), rep = gt2 / max(nitems, 1);
       const bool active = true;
       if (nitems > 0 && rep < nrep) {
         const int row = item >> 2, sg = item & 3, t = r0 + row;
         float v8[8];
+        if constexpr (TA) {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
+          const uint32_t zm = G.zmask[par] >> (8 * sg);
+          const float* zpv = zs_prev + (size_t)row * TS + 8 * sg;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v8[i] = 0.f;
+          for (int i = 0; i < 8; ++i) v8[i] = ((zm >> i) & 1u) ? 0.f : zpv[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v8[i] = 0.f;
+        }
         {  // fixed summation order c = 0 .. C-1 (results independent of the unrolling)
           int c = 0;
           for (; c + 4 <= C; c += 4) {
@@ -744,7 +827,7 @@ bool fits(int s) {
   return make_layout<KP, NG, NA>(C, (int)ceil_div(KP, C)).total <= kSmemLimit;
 }
 
-template <int KP, int NG, int NA>
+template <int KP, int NG, int NA, bool TA = false>
 int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k, double tol,
            double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz, float* E, int64_t lde,
            int32_t* iters, float* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st, bool query,
@@ -754,7 +837,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
   const Layout Lo = make_layout<KP, NG, NA>(C, rs);
   const size_t scale_bytes = (sizeof(float) * (size_t)(n_units > 0 ? n_units : 1) + 255) & ~(size_t)255;
   if (query) { *need = scale_bytes; return L1F_OK; }
-  auto kern = adm_tc_kernel<KP, NG, NA>;
+  auto kern = adm_tc_kernel<KP, NG, NA, TA>;
   static bool configured = false;
   if (!configured) {
     L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
@@ -859,6 +942,18 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
     case 128: L1F_TC(128, 1, 3); break;
     case 160: L1F_TC(160, 1, 3); break;
   }
+  // larger k: dictionary for phase a in TMEM (3 pieces), 2 pieces in shared memory for phase c
+#define L1F_TA(KP)                                                                                              \
+  if (fits<KP, 1, 2>(s))                                                                                         \
+    return launch<KP, 1, 2, true>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E,   \
+                                  lde, iters, res, status, workspace, ws_bytes, st, query, need)
+  switch ((int)l1f::ceil_div(k, 16) * 16) {
+    case 176: L1F_TA(176); break;
+    case 192: L1F_TA(192); break;
+    case 208: L1F_TA(208); break;
+    case 224: L1F_TA(224); break;
+  }
+#undef L1F_TA
   return L1F_ERR_UNSUPPORTED;
 #undef L1F_TC
   return L1F_ERR_UNSUPPORTED;

@@ -1,7 +1,8 @@
 """GPU: the tensor-core ADM filter (csrc/filter_tc.cu) against the FP64 oracle and the SIMT kernel.
 
-Covers both variants (two slot groups for k <= 112, one group with two phase-c M tiles for
-112 < k <= 160), cluster sizes 1..16, slot refills (many more units than slots) with dead units
+Covers the three variants (two slot groups for k <= 112; one group with two phase-c M tiles
+for 112 < k <= 160; one group with the phase-a dictionary in TMEM and the residual-form z step
+for 160 < k <= 224), cluster sizes 1..16, slot refills (many more units than slots) with dead units
 in between, the e output, max_iter status codes, and bitwise independence of unit order.
 Reference semantics: _solve_block, pkg/src/l1pcp/l1reg.py:59-137.  Gate (north_star, FP32):
 relative Frobenius difference of A z <= 1e-4; iteration counts within +-1 of the oracle for
@@ -47,7 +48,8 @@ def _run(x, a, tol=1e-7, max_iter=1000, want_e=False, tc=True):
 
 
 @pytest.mark.parametrize("s,k,n", [(100, 20, 50), (500, 48, 700), (1000, 100, 2500), (1000, 112, 400),
-                                   (2000, 100, 300), (1000, 128, 300), (1500, 150, 200), (777, 37, 900)])
+                                   (2000, 100, 300), (1000, 128, 300), (1500, 150, 200), (777, 37, 900),
+                                   (2000, 200, 700), (1800, 176, 300), (2048, 224, 100)])
 def test_tc_filter_matches_oracle(s, k, n):
     rng = np.random.default_rng(s + 7 * k + n)
     a, x = _units(rng, s, k, n)
@@ -97,7 +99,7 @@ def test_tc_agrees_with_simt_kernel():
     assert (np.abs(it_tc.numpy().astype(int) - it_si.numpy().astype(int)) <= 1).mean() >= 0.97
 
 
-@pytest.mark.parametrize("k", [64, 150])
+@pytest.mark.parametrize("k", [64, 150, 200])
 def test_tc_results_independent_of_unit_order(k):
     rng = np.random.default_rng(k)
     a, x = _units(rng, 640, k, 700)
