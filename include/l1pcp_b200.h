@@ -163,6 +163,10 @@ int l1f_soft_threshold(int dtype, const void* X, void* Y, int64_t count, double 
  * Seed-stage dense kernels (FP64) — the small PCP of `recover_seed` (l1filter.py:90-113).
  *  l1f_svd_f64: thin SVD W = U diag(sigma) V^T, p = min(m,n), sigma descending
  *     (matcore.py:73-88 before the rank cut).  U m x p, V n x p, row-major.
+ *  l1f_svd_gram_f64: the same outputs through the eigendecomposition of the smaller Gram
+ *     matrix (the seed's final factorisation, l1filter.py:90-113): columns with sigma_i above
+ *     ~sqrt(eps) * sigma_max are accurate to ~eps * sigma_max / sigma_i; smaller ones are noise
+ *     (below the seed's rank cut of 1e-6 * sigma_max).
  *  l1f_spectral_norm_f64: 25-step power iteration from the all-ones vector
  *     (pcp_adm.py:69-87); result to *out_host.
  *  l1f_svt_f64: out = U max(sigma - eta, 0) V^T and *rank_host = #(sigma > eta)
@@ -173,6 +177,8 @@ int l1f_soft_threshold(int dtype, const void* X, void* Y, int64_t count, double 
  * ---------------------------------------------------------------------------------- */
 int l1f_svd_f64(const double* W, int64_t m, int64_t n, int64_t ldw,
                 double* U, double* sigma, double* V, void* stream);
+int l1f_svd_gram_f64(const double* W, int64_t m, int64_t n, int64_t ldw,
+                     double* U, double* sigma, double* V, void* stream);
 int l1f_spectral_norm_f64(const double* M, int64_t m, int64_t n, int32_t iters,
                           double* out_host, void* stream);
 int l1f_svt_f64(const double* W, int64_t m, int64_t n, double eta, double* out,

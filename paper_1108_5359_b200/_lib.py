@@ -72,6 +72,7 @@ SIGNATURES = {
     "l1f_diff_norms": (_int, [_int, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
     "l1f_soft_threshold": (_int, [_int, _vp, _vp, _i64, _f64, _vp]),
     "l1f_svd_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "l1f_svd_gram_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "l1f_spectral_norm_f64": (_int, [_vp, _i64, _i64, _i32, _vp, _vp]),
     "l1f_svt_f64": (_int, [_vp, _i64, _i64, _f64, _vp, _vp, _vp]),
     "l1f_pcp_f64": (_int, [_vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp,

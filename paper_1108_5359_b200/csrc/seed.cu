@@ -382,6 +382,91 @@ extern "C" int l1f_spectral_norm_f64(const double* M, int64_t m, int64_t n, int3
   return spectral_norm(h, M, m, n, iters, out_host, st);
 }
 
+// Thin SVD through the eigendecomposition of the smaller Gram matrix (the seed's final
+// factorisation, l1filter.py:90-113 -> matcore.svd).  For a kept singular triplet (sigma_i >
+// rank_tol * sigma_max) the computed U (or V) column is orthonormal to ~eps * sigma_max /
+// sigma_i; sigma below ~sqrt(eps) * sigma_max are not resolved (they are cut as noise).
+__global__ void eig_desc_rowmajor_kernel(const double* __restrict__ G, int p, double* __restrict__ out) {
+  // out (p x p row-major)[i][j] = eigenvector j in descending order, component i
+  const int64_t total = (int64_t)p * p;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / p, j = e - i * p;
+    out[e] = G[(int64_t)(p - 1 - j) * p + i];
+  }
+}
+__global__ void sigma_from_eig_kernel(const double* __restrict__ lam, int p, double* __restrict__ sig,
+                                      double* __restrict__ inv) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p; j += gridDim.x * blockDim.x) {
+    const double l = lam[p - 1 - j];
+    const double sg = l > 0.0 ? sqrt(l) : 0.0;
+    sig[j] = sg;
+    inv[j] = sg > 0.0 ? 1.0 / sg : 0.0;
+  }
+}
+
+static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sig, double* V,
+                    cudaStream_t st) {
+  const bool right = n <= m;
+  const int p = (int)(right ? n : m), q = (int)(right ? m : n);
+  Buf g(st), ev(st), work(st), info(st), inv(st);
+  L1F_CUDA_TRY(g.alloc(sizeof(double) * (size_t)p * p));
+  L1F_CUDA_TRY(ev.alloc(sizeof(double) * (size_t)p));
+  L1F_CUDA_TRY(inv.alloc(sizeof(double) * (size_t)p));
+  const double one = 1.0, zero = 0.0;
+  cublasSetPointerMode(h->blas, CUBLAS_POINTER_MODE_HOST);
+  // row-major W (m x n, ld ldw) == column-major X = W^T (n x m, ld ldw)
+  if (right) cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)ldw, &zero, g.d(), p);
+  else cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)ldw, &zero, g.d(), p);
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
+                                  &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("syevd_bufferSize failed");
+    return L1F_ERR_CUDA;
+  }
+  L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
+  L1F_CUDA_TRY(info.alloc(sizeof(int)));
+  if (cusolverDnDsyevd(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
+                       (int*)info.p) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("cusolverDnDsyevd failed");
+    return L1F_ERR_SVD;
+  }
+  int info_h = 0;
+  L1F_CUDA_TRY(cudaMemcpyAsync(&info_h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  if (info_h != 0) {
+    set_error("SVD (Gram) failed on (%lld, %lld) matrix: syevd info %d", (long long)m, (long long)n, info_h);
+    return L1F_ERR_SVD;
+  }
+  sigma_from_eig_kernel<<<(p + 255) / 256, 256, 0, st>>>(ev.d(), p, sig, inv.d());
+  const int blocks = num_sms() * 4;
+  if (right) {
+    // V (n x p row-major) = eigenvectors; U (m x p row-major) = W V diag(1/sigma):
+    // column-major U^T (p x m) = V^T (col-major view of V) * W^T (col-major view of W)
+    eig_desc_rowmajor_kernel<<<blocks, 256, 0, st>>>(g.d(), p, V);
+    cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, (int)m, (int)n, &one, V, p, W, (int)ldw, &zero, U, p);
+    scale_cols_kernel<<<blocks, 256, 0, st>>>(U, m, p, p, inv.d());
+  } else {
+    // U (m x p row-major) = eigenvectors; V (n x p row-major) = W^T U diag(1/sigma):
+    // column-major V^T (p x n) = U^T (col-major view of U) * W (transpose of the col-major view)
+    eig_desc_rowmajor_kernel<<<blocks, 256, 0, st>>>(g.d(), p, U);
+    cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_T, p, (int)n, (int)m, &one, U, p, W, (int)ldw, &zero, V, p);
+    scale_cols_kernel<<<blocks, 256, 0, st>>>(V, n, p, p, inv.d());
+  }
+  L1F_CHECK_LAUNCH();
+  return L1F_OK;
+}
+
+extern "C" int l1f_svd_gram_f64(const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sigma,
+                                double* V, void* stream) {
+  L1F_REQUIRE(m >= 1 && n >= 1 && ldw >= n, L1F_ERR_ARG, "svd_gram: bad shape");
+  L1F_REQUIRE(m < INT32_MAX && n < INT32_MAX, L1F_ERR_UNSUPPORTED, "svd_gram: matrix too large");
+  Handles* h;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  return svd_gram(h, W, m, n, ldw, U, sigma, V, st);
+}
+
 extern "C" int l1f_svt_f64(const double* W, int64_t m, int64_t n, double eta, double* out, int32_t* rank_host,
                            void* stream) {
   L1F_REQUIRE(m >= 1 && n >= 1, L1F_ERR_ARG, "svt: bad shape");

@@ -12,6 +12,7 @@ benchmark.  All matrices are CUDA tensors; every arithmetic step is a C-ABI kern
 """
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -71,11 +72,14 @@ def gather(mt, rows, cols, out_dtype=None, transpose=False):
     return out
 
 
-def svd_device(t):
+def svd_device(t, gram=False):
+    """Thin SVD of a float64 CUDA matrix; gram=True uses the Gram-eigendecomposition path
+    (l1f_svd_gram_f64, for the seed's rank-revealing factorisation)."""
     m, n = t.shape
     p = min(m, n)
     u, s, v = dv.empty((m, p)), dv.empty((p,)), dv.empty((n, p))
-    _lib.call("l1f_svd_f64", dv.ptr(t), m, n, t.stride(0), dv.ptr(u), dv.ptr(s), dv.ptr(v), dv.stream(),
+    fn = "l1f_svd_gram_f64" if gram else "l1f_svd_f64"
+    _lib.call(fn, dv.ptr(t), m, n, t.stride(0), dv.ptr(u), dv.ptr(s), dv.ptr(v), dv.stream(),
               what=f"SVD failed on {tuple(t.shape)} matrix")
     return u, s, v
 
@@ -87,7 +91,9 @@ def recover_seed_device(block, adm=None, rank_tol=1e-6):
     cfg = AdmConfig(lam=lam, tol=adm.tol, beta0=adm.beta0, rho=adm.rho, beta_max=adm.beta_max,
                     max_iter=adm.max_iter)
     l, _, info = solve_pcp_device(block, cfg)
-    u, s, v = svd_device(l)
+    # the seed L is exactly low rank (the last SVT), so the Gram route resolves every kept
+    # triplet; L1F_SEED_SVD=gesvd restores the full SVD
+    u, s, v = svd_device(l, gram=os.environ.get("L1F_SEED_SVD", "gram") != "gesvd")
     sh = s.cpu().numpy()
     cutoff = rank_tol * (sh[0] if sh.size else 0.0)
     k = int((sh > cutoff).sum())

@@ -239,3 +239,23 @@ def test_sharded_cuda_backend_matches_single_gpu_solve():
     sol = l1pcp.estimate_rank_and_solve(mt, l1pcp.FilterConfig(rank_hint=5, rng_seed=0, adm=adm))
     assert info["k"] == sol.rank_of_l == 5
     assert torch.equal(l, sol.l) and torch.equal(s, sol.s)
+
+
+@pytest.mark.parametrize("m,n,r", [(300, 300, 20), (500, 200, 30), (150, 400, 10)])
+def test_svd_gram_matches_gesvd_on_low_rank(m, n, r):
+    """l1f_svd_gram_f64 (the seed's final factorisation) vs l1f_svd_f64 on an exactly rank-r
+    matrix: singular values, the projectors U U^T / V V^T and orthonormality of the kept triplets."""
+    rng = np.random.default_rng(m + n + r)
+    x = rng.standard_normal((m, r)) @ np.diag(np.linspace(1.0, 50.0, r)) @ rng.standard_normal((r, n))
+    t = torch.from_numpy(x).cuda()
+    u1, s1, v1 = engine.svd_device(t)
+    u2, s2, v2 = engine.svd_device(t, gram=True)
+    s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
+    np.testing.assert_allclose(s2[:r], s1[:r], rtol=1e-11)
+    assert (s2[r:] <= 1e-6 * s2[0]).all()
+    for a, b in ((u1, u2), (v1, v2)):
+        a, b = a[:, :r].cpu().numpy(), b[:, :r].cpu().numpy()
+        assert np.abs(a @ a.T - b @ b.T).max() <= 1e-10
+        assert np.abs(b.T @ b - np.eye(r)).max() <= 1e-10
+    rec = (u2[:, :r] * torch.from_numpy(s2[:r]).cuda()) @ v2[:, :r].T
+    assert torch.linalg.norm(rec - t) <= 1e-11 * torch.linalg.norm(t)
