@@ -73,7 +73,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -241,10 +241,10 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or os.environ.get("L1F_FORCE_SHARDED") == "1":  # the latter: test the N-GPU driver on 1 GPU
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1108_5359_b200 import distributed as pdist
-        return pdist.run_bench(args, rank, world)
+        return pdist.run_bench(args, rank, world, clock_sampler=ClockSampler)
 
     cfgd = cfg_of(args.config)
     m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]

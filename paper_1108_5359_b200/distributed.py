@@ -17,6 +17,7 @@ world size.  Compute goes through a backend object (``CudaBackend`` in productio
 kernels over NCCL tensors); tests substitute a CPU backend under gloo to check the plumbing.
 """
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -196,8 +197,87 @@ class _FactorPlan:
         self.d_col_idx = engine.index_tensor(plan.col_idx)
 
 
-def run_bench(args, rank, world):
-    """bench.py --gpus N: strong scaling of one synthetic matrix over N GPUs (NCCL)."""
+class CudaShardedStep:
+    """The timed multi-GPU step on CUDA, with everything that does not depend on M's values
+    prepared once (index tensors, cast seed factors, factor slices, workspaces, outputs) so the
+    step enqueues without host synchronisation.  Same exchanges and per-unit arithmetic as
+    solve_from_seed with CudaBackend (bitwise identical L, S)."""
+
+    def __init__(self, m_local, plan, adm, u, sig, v, group=None):
+        from . import _device as dv
+        from . import _lib, engine
+        self.dv, self.lib, self.e = dv, _lib, engine
+        self.plan, self.adm, self.group = plan, adm, group
+        self.k = int(sig.shape[0])
+        dt = m_local.dtype
+        self.dt, self.fdt = dt, engine.filter_dtype_for(self.k, dt)
+        self.u64, self.sig, self.v64 = u, sig, v
+        self.u, self.v = u.to(self.fdt).contiguous(), v.to(self.fdt).contiguous()
+        idx = engine.index_tensor
+        self.d_seed_local = idx(plan.row_idx[plan.my_seed_pos] - plan.r0)
+        self.seed_counts = [int((plan.seed_owner == g).sum()) for g in range(plan.world)]
+        self.col_counts = [c1 - c0 for c0, c1 in plan.col_units]
+        self.d_my_cols = idx(plan.my_cols)
+        self.d_my_rows_local = idx(plan.my_rows - plan.r0)
+        self.d_col_idx = idx(plan.col_idx)
+        loc = (plan.row_idx >= plan.r0) & (plan.row_idx < plan.r1)
+        self.d_local_seed_rows = idx(plan.row_idx[loc] - plan.r0)
+        self.n_local_seed = int(loc.sum())
+        self.u_local = u[idx(np.flatnonzero(loc))].contiguous()
+        rows = plan.r1 - plan.r0
+        self.af = torch.empty((rows, self.k), dtype=dt, device="cuda")
+        self.bf = torch.empty((plan.n, self.k), dtype=dt, device="cuda")
+        self.l = torch.empty_like(m_local)
+        self.s = torch.empty_like(m_local)
+        self.xc = torch.empty((len(plan.my_cols), len(plan.row_idx)), dtype=self.fdt, device="cuda")
+        self.xr = torch.empty((len(plan.my_rows), len(plan.col_idx)), dtype=self.fdt, device="cuda")
+        code = _lib.F32 if self.fdt == torch.float32 else _lib.F64
+        nbytes = max(_lib.load().l1f_filter_workspace_bytes(code, len(plan.row_idx), self.k, max(1, len(plan.my_cols))),
+                     _lib.load().l1f_filter_workspace_bytes(code, len(plan.col_idx), self.k, max(1, len(plan.my_rows))))
+        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+        self.launches_per_step = 11  # 2 gathers, 2 x (scale prologue + filter), factors, 2 pads, reconstruct, sum
+
+    def step(self, m_local, events=None):
+        from .l1reg import filter_units
+        dv, lib, p = self.dv, self.lib, self.plan
+        local = m_local[self.d_seed_local]
+        seed_rows = _all_gather_rows(local, self.seed_counts, self.group)   # exchange 1
+        code_in = dv.dtype_code(m_local)
+        code_f = lib.F32 if self.fdt == torch.float32 else lib.F64
+        lib.call("l1f_gather", dv.dtype_code(seed_rows), dv.ptr(seed_rows), seed_rows.stride(0), None,
+                 seed_rows.shape[0], dv.ptr(self.d_my_cols), len(p.my_cols), code_f, dv.ptr(self.xc),
+                 self.xc.stride(0), 1, dv.stream())
+        lib.call("l1f_gather", code_in, dv.ptr(m_local), m_local.stride(0), dv.ptr(self.d_my_rows_local),
+                 len(p.my_rows), dv.ptr(self.d_col_idx), len(p.col_idx), code_f, dv.ptr(self.xr), self.xr.stride(0), 0,
+                 dv.stream())
+        if events is not None:
+            events[0].record()
+        zc, _, itc, _, stc = filter_units(self.xc, self.u, self.adm, want_e=False, workspace=self.ws)
+        zr, _, itr, _, st_r = filter_units(self.xr, self.v, self.adm, want_e=False, workspace=self.ws)
+        if events is not None:
+            events[1].record()
+        if self.fdt != self.dt:
+            zc, zr = zc.to(self.dt), zr.to(self.dt)
+        zc_all = _all_gather_rows(zc, self.col_counts, self.group)           # exchange 2: Q~
+        code = lib.F32 if self.dt == torch.float32 else lib.F64
+        lib.call("l1f_build_factors", code, p.r1 - p.r0, p.n, self.k, dv.ptr(self.d_local_seed_rows),
+                 self.n_local_seed, dv.ptr(self.d_col_idx), len(p.col_idx), dv.ptr(self.u_local), dv.ptr(self.sig),
+                 dv.ptr(self.v64), dv.ptr(zc_all), zc_all.stride(0), dv.ptr(zr), max(zr.stride(0), self.k),
+                 dv.ptr(self.af), dv.ptr(self.bf), dv.stream())
+        self.e.reconstruct(m_local, self.af, self.bf, self.l, self.s)
+        dev = m_local.device
+        it = torch.stack([itc.max() if itc.numel() else torch.zeros((), dtype=itc.dtype, device=dev),
+                          itr.max() if itr.numel() else torch.zeros((), dtype=itr.dtype, device=dev)]).max()
+        failed = ((stc == 1) | (stc == 2)).sum() + ((st_r == 1) | (st_r == 2)).sum()
+        stats = torch.stack([it.double(), failed.double(),
+                             torch.tensor(float(itc.numel() + itr.numel()), dtype=torch.float64, device=dev),
+                             itc.double().sum() + itr.double().sum()])
+        return self.l, self.s, stats, (itc, itr)
+
+
+def run_bench(args, rank, world, clock_sampler=None):
+    """bench.py --gpus N: strong scaling of one synthetic matrix over N GPUs (NCCL).  Same
+    contract keys as the 1-GPU line; times are the max over ranks of CUDA-event times."""
     import json
 
     import paper_1108_5359_b200 as l1pcp
@@ -217,36 +297,96 @@ def run_bench(args, rank, world):
     adm = l1pcp.AdmConfig(tol=tol)
     backend = CudaBackend()
     # seed (t1, outside the timed steps as on one GPU): rank 0 solves, factors broadcast
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     seed_rows = gather_seed_rows(m_local, plan)
     u, sig, v, _ = seed_factors(seed_rows, plan, backend, adm)
     torch.cuda.synchronize()
     t1 = time.perf_counter() - t0
     del seed_rows
-    for _ in range(max(1, args.warmup)):
-        solve_from_seed(m_local, plan, backend, adm, u, sig, v)
+    stepper = CudaShardedStep(m_local, plan, adm, u, sig, v)
+    for _ in range(max(3, args.warmup)):
+        stepper.step(m_local)
     torch.cuda.synchronize()
     dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = clock_sampler(int(os.environ.get("LOCAL_RANK", "0"))) if clock_sampler else None
+    if sampler:
+        sampler.__enter__()
+    torch.cuda.synchronize()
     start.record()
-    for _ in range(args.steps):
-        l_local, s_local, info = solve_from_seed(m_local, plan, backend, adm, u, sig, v)
+    for i in range(args.steps):
+        l_local, s_local, stats, (itc, itr) = stepper.step(m_local, evs[i])
+        dist.all_reduce(stats, group=None)  # statistics (exchange 3); sum over ranks
     end.record()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__(None, None, None)
     dist.barrier()
-    ms = torch.tensor([start.elapsed_time(end) / args.steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    filt_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    its = float((itc.double().sum() + itr.double().sum()).item())
+    t = torch.tensor([start.elapsed_time(end) / args.steps, filt_ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    flops = torch.tensor([its * len(row_idx) * (4 * stepper.k + 12)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(flops)  # algorithmic filter work of all ranks (s_r = s_c here)
+    # e2e: each rank's row block from pinned host memory, L and S back to pinned host memory
+    m_host = torch.empty(m_local.shape, dtype=m_local.dtype, pin_memory=True)
+    m_host.copy_(m_local)
+    l_host = torch.empty_like(m_host, pin_memory=True)
+    s_host = torch.empty_like(m_host, pin_memory=True)
+    m_dev = torch.empty_like(m_local)
+    e_steps = max(1, min(args.steps, 3))
+
+    def e2e_step():
+        m_dev.copy_(m_host, non_blocking=True)
+        l_d, s_d, st, _ = stepper.step(m_dev)
+        l_host.copy_(l_d, non_blocking=True)
+        s_host.copy_(s_d, non_blocking=True)
+        dist.all_reduce(st)
+        return st
+
+    e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(e_steps):
+        st = e2e_step()
+        st_host = st.cpu()  # device -> host read of the step's result
+    b.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([a.elapsed_time(b) / e_steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    stats_h = stats.cpu().numpy()
     if rank == 0:
-        ms_v = float(ms.item())
+        ms_v, filt_v = float(t[0].item()), float(t[1].item())
+        fma = engine.fma_peak_tflops()
+        ach = float(flops.item()) / (filt_v * 1e-3) / 1e12
+        nbytes = m * n * m_local.element_size()
         line = {"metric": "M entries/s (m*n / solve time)", "value": m * n / (ms_v * 1e-3) / 1e6, "unit": "M entries/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v,
+                "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_v,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (Philox, row shards generated per rank)",
-                "config": {"workload": f"{cfgd['name']}: {m}x{n} r={r}", "parallelism": f"row-sharded x{world}",
-                           "collectives": "all-gather seed rows, broadcast seed factors, all-gather Q~, "
-                                          "all-reduce stats (NCCL)"},
-                "phases_ms": {"t1_seed_s": t1}, "gpu_launches": None,
-                "filter": {kk: vv for kk, vv in info.items() if kk != "times"}}
+                "config": {"workload": f"{cfgd['name']}: {m}x{n} r={r}", "m": m, "n": n, "rank": r,
+                           "parallelism": f"row-sharded x{world}",
+                           "collectives": "all-gather seed rows, all-gather Q~, all-reduce stats (NCCL); seed factors "
+                                          "broadcast once",
+                           "l2": "inputs larger than L2 (row block %.2f GB per GPU)" % (nbytes / world / 1e9)},
+                "roofline": {"bound": "fp32", "kernel": "adm_tc_kernel (column + row filters, max over ranks)",
+                             "achieved": ach, "peak": fma * world, "unit": "TFLOP/s", "frac": ach / (fma * world),
+                             "peak_source": "measured FP32 FMA probe x N GPUs", "traffic": None,
+                             "kernel_ms_per_step": filt_v},
+                "phases_ms": {"t1_seed_s": t1, "filters": filt_v},
+                "filter": {"units": int(stats_h[2]), "mean_iters": float(stats_h[3] / max(stats_h[2], 1)),
+                           "max_iters_summed_over_ranks": int(stats_h[0]), "failed_units": int(stats_h[1])},
+                "gpu_launches": stepper.launches_per_step * args.steps * world,
+                "gpu_launches_per_rank": stepper.launches_per_step * args.steps,
+                "clocks": sampler.summary() if sampler else None,
+                "e2e": {"value": m * n / (float(te.item()) * 1e-3) / 1e6, "unit": "M entries/s",
+                        "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 2 * nbytes,
+                        "ms_per_step": float(te.item()), "steps": e_steps,
+                        "path": "per rank: pinned host row block -> H2D -> sharded step -> D2H of L, S rows"}}
         print(json.dumps(line))
     dist.destroy_process_group()
     return 0
