@@ -683,7 +683,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const int sl = __ffs(mm) - 1;
         const int64_t u = G.unit[sl];
         for (int row = lane; row < vmine; row += 32)
-          if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zs_prev[row * TS + sl];
+          if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zs_prev[row * TS + 4 * ((sl >> 2) ^ (row & 7)) + (sl & 3)];
       }
       __syncwarp();
       if (lane == 0) {
@@ -709,13 +709,18 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       const int item = gt2 % max(nitems, 1), rep = gt2 / max(nitems, 1);
       const bool active = true;
       if (nitems > 0 && rep < nrep) {
-        const int row = item >> 2, sg = item & 3, t = r0 + row;
+        // slot-group-major items: consecutive lanes take consecutive rows of one slot group, so the
+        // swizzled inbox/slice accesses and the z-operand stores are bank-conflict free
+        const int sg = item / vmine, row = item - sg * vmine, t = r0 + row;
         float v8[8];
         if constexpr (TA) {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
           const uint32_t zm = G.zmask[par] >> (8 * sg);
-          const float* zpv = zs_prev + (size_t)row * TS + 8 * sg;
+          const float* zrow = zs_prev + (size_t)row * TS;
+          const float4 p0 = *reinterpret_cast<const float4*>(zrow + 4 * ((2 * sg) ^ (row & 7)));
+          const float4 p1 = *reinterpret_cast<const float4*>(zrow + 4 * ((2 * sg + 1) ^ (row & 7)));
+          const float zv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v8[i] = ((zm >> i) & 1u) ? 0.f : zpv[i];
+          for (int i = 0; i < 8; ++i) v8[i] = ((zm >> i) & 1u) ? 0.f : zv[i];
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) v8[i] = 0.f;
@@ -752,9 +757,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
         stamp(8);
         if (active && rep == 0) {
-          float* dz = zs_cur + (size_t)row * TS + 8 * sg;
-          *reinterpret_cast<float4*>(dz) = make_float4(v8[0], v8[1], v8[2], v8[3]);
-          *reinterpret_cast<float4*>(dz + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
+          float* dz = zs_cur + (size_t)row * TS;  // 16-byte chunks XOR-swizzled by (row & 7)
+          *reinterpret_cast<float4*>(dz + 4 * ((2 * sg) ^ (row & 7))) = make_float4(v8[0], v8[1], v8[2], v8[3]);
+          *reinterpret_cast<float4*>(dz + 4 * ((2 * sg + 1) ^ (row & 7))) = make_float4(v8[4], v8[5], v8[6], v8[7]);
           *reinterpret_cast<uint4*>(zop + off) = w0;
           *reinterpret_cast<uint4*>(zop + 4 * 64 + off) = w1;
           *reinterpret_cast<uint4*>(zop + 8 * 64 + off) = w2;
