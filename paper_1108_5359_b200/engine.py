@@ -165,7 +165,8 @@ SMALL_K_FP64 = 16
 
 
 def filter_dtype_for(k, dtype):
-    return torch.float64 if k <= SMALL_K_FP64 else dtype
+    limit = int(os.environ.get("L1F_SMALL_K_FP64", SMALL_K_FP64))
+    return torch.float64 if k <= limit else dtype
 
 
 class FilterPlan:
