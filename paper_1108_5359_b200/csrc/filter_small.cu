@@ -256,6 +256,10 @@ int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T*
     if (s <= 64) L1F_SMALL(8, 4, 16);
     if (s <= 128) L1F_SMALL(8, 8, 16);
     if (s <= 256) L1F_SMALL(8, 8, 32);
+  } else if (k <= 10) {  // configs 1 and 4 (k = 10, s = 100): exact width, 8-lane groups
+    if (s <= 104) L1F_SMALL(10, 13, 8);
+    if (s <= 128) L1F_SMALL(10, 8, 16);
+    if (s <= 256) L1F_SMALL(10, 8, 32);
   } else if (k <= 12) {
     if (s <= 64) L1F_SMALL(12, 4, 16);
     if (s <= 128) L1F_SMALL(12, 8, 16);
