@@ -111,3 +111,53 @@ def test_tc_results_independent_of_unit_order(k):
             assert torch.equal(f[torch.from_numpy(perm)], p)
     sub = _run(x[:, 100:140], a)
     assert torch.equal(sub[0], full[0][100:140])
+
+
+def test_tc_filter_few_units_many_slots():
+    # C = 8 CTAs, 2 groups x 32 slots, only 3 units: nearly every slot of both groups is empty
+    rng = np.random.default_rng(21)
+    a, x = _units(rng, 1000, 100, 3)
+    zr, er, itr, rr, sr = adm_filter.solve_units(x, a, 1e-7)
+    z, e, it, res, st = _run(x, a)
+    assert np.linalg.norm(a @ z.double().numpy().T - a @ zr) <= 1e-4 * np.linalg.norm(a @ zr)
+    assert (np.abs(it.numpy().astype(int) - itr.astype(int)) <= 1).all()
+
+
+@pytest.mark.parametrize("k", [100, 200])
+def test_tc_filter_explicit_beta_and_rho(k):
+    rng = np.random.default_rng(k + 1)
+    a, x = _units(rng, 2 * k if k > 100 else 1000, k, 150)
+    cfg = dict(tol=1e-7, rho=1.3, beta0=0.01, beta_max=500.0)
+    zr, er, itr, rr, sr = adm_filter.solve_units(x, a, cfg["tol"], rho=cfg["rho"], beta0=cfg["beta0"],
+                                                 beta_max=cfg["beta_max"])
+    xt = torch.from_numpy(np.ascontiguousarray(x.T, dtype=np.float32)).cuda()
+    at = torch.from_numpy(a.astype(np.float32)).cuda()
+    z, e, it, res, st = filter_units(xt, at, l1pcp.AdmConfig(**cfg), want_e=False)
+    lc, lr = a @ z.double().cpu().numpy().T, a @ zr
+    assert np.linalg.norm(lc - lr) <= 1e-4 * np.linalg.norm(lr)
+    assert (np.abs(it.cpu().numpy().astype(int) - itr.astype(int)) <= 1).mean() >= 0.95
+
+
+def test_tc_filter_strided_abi():
+    # leading dimensions larger than the logical widths (X, A and Z with padding)
+    import ctypes
+    from paper_1108_5359_b200 import _device as dv
+    rng = np.random.default_rng(9)
+    s, k, n = 1000, 100, 120
+    a, x = _units(rng, s, k, n)
+    xp = torch.zeros((n, s + 7), dtype=torch.float32, device="cuda")
+    xp[:, :s] = torch.from_numpy(x.T.astype(np.float32)).cuda()
+    ap = torch.zeros((s, k + 5), dtype=torch.float32, device="cuda")
+    ap[:, :k] = torch.from_numpy(a.astype(np.float32)).cuda()
+    zp = torch.full((n, k + 3), 7.0, dtype=torch.float32, device="cuda")
+    iters = torch.empty(n, dtype=torch.int32, device="cuda")
+    res = torch.empty(n, dtype=torch.float32, device="cuda")
+    status = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.call("l1f_filter_f32", dv.ptr(xp), xp.stride(0), s, n, dv.ptr(ap), ap.stride(0), k, 1e-7, 1.5, 0.0, 0.0,
+              1000, dv.ptr(zp), zp.stride(0), None, s, dv.ptr(iters), dv.ptr(res), dv.ptr(status), None, 0,
+              dv.stream())
+    torch.cuda.synchronize()
+    zr, er, itr, rr, sr = adm_filter.solve_units(x, a, 1e-7)
+    z = zp[:, :k].double().cpu().numpy()
+    assert np.linalg.norm(a @ z.T - a @ zr) <= 1e-4 * np.linalg.norm(a @ zr)
+    assert (zp[:, k:] == 7.0).all()  # padding untouched
