@@ -3,8 +3,9 @@
 //
 // Reference: _solve_block, pkg/src/l1pcp/l1reg.py:59-137 (per-unit ADM for min ||x - A z||_1).
 // A cluster of C = ceil(s / 128) CTAs keeps the s x k dictionary resident (CTA c: rows
-// [128 c, 128 c + 128)).  Each CTA runs TWO independent slot groups of 32 units (warps 0-7 and
-// 8-15); a group's pass is one ADM iteration of its 32 units:
+// [128 c, 128 c + 128)).  Each CTA runs NG independent slot groups of 32 units (NG = 2 for
+// k <= 112: warps 0-7 and 8-15; NG = 1 for larger k); a group's pass is one ADM iteration of its
+// 32 units:
 //   phase a   az[row][slot] = sum_t A[row][t] z[t][slot]      tcgen05.mma M=128 (rows) N=32 K=k
 //   phase b   the elementwise ADM update of filter_resident.cu (cancellation-free residual)
 //   phase c   zp[t][slot]   = sum_row A[row][t] v[row][slot]   tcgen05.mma M=128 (t)    N=32 K=128
@@ -17,14 +18,17 @@
 //
 // FP32 accuracy from BF16 tensor cores: every operand is split into three bf16 pieces
 // x = x0 + x1 + x2 (each the bf16 rounding of the remainder; 24 significant bits) and the
-// products with i + j <= 2 are accumulated in FP32 in TMEM (6 MMAs per K step; the dropped terms
-// are ~2^-26 relative).  bf16 because tcgen05 reads bf16 operands in MN-major layout (TF32 only
+// products with i + j <= 2 are accumulated in FP32 in TMEM (the dropped terms are ~2^-26
+// relative).  The z / v operand holds its pieces side by side along N, so one MMA per dictionary
+// piece and K step computes a0 [z0 z1 z2], a1 [z0 z1], a2 [z0] into three column blocks that hold
+// the products of order 0, 1 and 2 (summed after tcgen05.ld).  bf16 because tcgen05 reads bf16 operands in MN-major layout (TF32 only
 // K-major, tools/umma_debug.cu): the dictionary's no-swizzle core matrices (8 rows x 8 columns,
 // 16-byte rows) are K-major for phase a (M = rows) and MN-major for phase c (M = columns), so ONE
 // resident copy of A (3 pieces, 6 B per element) serves both contractions.
 //
-// Roles in a group (8 warps): warp 1 lane 0 issues the MMAs, warp 0 takes the per-slot decisions,
-// all 8 warps do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows, slots 16 (w / 4) .. +15).
+// Roles in a group: warp 1 lane 0 issues the MMAs, warp 0 takes the per-slot decisions, all warps
+// do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows; 16 slots per thread at NG = 2, 8 at
+// NG = 1).  Profiling: L1F_TC_PROF=1 prints clock64 phase times of one thread (CTA 0, group 0).
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -707,7 +711,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       const int nitems = vmine * 4;
       const int nrep = nitems > 0 ? min(4, max(1, (GT - 32) / nitems)) : 1;  // each re-reads all C partials
       const int item = gt2 % max(nitems, 1), rep = gt2 / max(nitems, 1);
-      const bool active = true;
       if (nitems > 0 && rep < nrep) {
         // slot-group-major items: consecutive lanes take consecutive rows of one slot group, so the
         // swizzled inbox/slice accesses and the z-operand stores are bank-conflict free
@@ -756,7 +759,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         split8(v8, w0, w1, w2);
         const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
         stamp(8);
-        if (active && rep == 0) {
+        if (rep == 0) {
           float* dz = zs_cur + (size_t)row * TS;  // 16-byte chunks XOR-swizzled by (row & 7)
           *reinterpret_cast<float4*>(dz + 4 * ((2 * sg) ^ (row & 7))) = make_float4(v8[0], v8[1], v8[2], v8[3]);
           *reinterpret_cast<float4*>(dz + 4 * ((2 * sg + 1) ^ (row & 7))) = make_float4(v8[4], v8[5], v8[6], v8[7]);
@@ -766,7 +769,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         }
         const uint32_t a0 = umma::saddr(zop + off), a1 = umma::saddr(zop + 4 * 64 + off),
                        a2 = umma::saddr(zop + 8 * 64 + off);
-        for (int d = rep; active && d < C - 1; d += nrep) {
+        for (int d = rep; d < C - 1; d += nrep) {
           const int peer = d < crank ? d : d + 1;
           const uint32_t pb = peer_addr(bar_r, peer);
           st_async16u(peer_addr(a0, peer), w0, pb);
