@@ -37,7 +37,7 @@ TOL = 1e-7  # BASELINE.json: ALM tolerance 1e-7
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])

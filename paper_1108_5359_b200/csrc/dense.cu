@@ -426,13 +426,24 @@ template <typename Ti, typename To>
 __global__ void gather_kernel(const Ti* __restrict__ M, int64_t ldm, const int64_t* __restrict__ rows,
                               int64_t nr, const int64_t* __restrict__ cols, int64_t nc,
                               To* __restrict__ out, int64_t ldo) {
-  const int64_t total = nr * nc;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / nc, c = e - r * nc;
-    const int64_t sr = rows ? rows[r] : r, sc = cols ? cols[c] : c;
-    out[r * ldo + c] = (To)M[sr * ldm + sc];
+  // thread = output column (its source column index kept in a register); blocks stride over rows
+  // with the row index broadcast; 4 rows per step keep several scattered loads in flight
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int64_t sc = cols ? cols[c] : c;
+  const int64_t step = gridDim.y;
+  int64_t r = blockIdx.y;
+  for (; r + 3 * step < nr; r += 4 * step) {
+    Ti v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t rr = r + u * step;
+      v[u] = M[(rows ? rows[rr] : rr) * ldm + sc];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[(r + u * step) * ldo + c] = (To)v[u];
   }
+  for (; r < nr; r += step) out[r * ldo + c] = (To)M[(rows ? rows[r] : r) * ldm + sc];
 }
 
 // out[c][r] = M[rows[r]][cols[c]] through a 32x32 shared-memory transpose
@@ -698,7 +709,10 @@ extern "C" int l1f_gather(int dtype_in, const void* M, int64_t ldm, const int64_
     gather_t_kernel<TI, TO><<<grid, 256, 0, st>>>((const TI*)M, ldm, rows, n_rows, cols, n_cols,    \
                                                   (TO*)out, ldo);                                    \
   } else {                                                                                           \
-    gather_kernel<TI, TO><<<grid_for(n_rows * n_cols, 256), 256, 0, st>>>(                          \
+    gather_kernel<TI, TO><<<dim3((unsigned)ceil_div(n_cols, 256),                                     \
+                             (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_rows,                     \
+                                 ceil_div((int64_t)num_sms() * 16, ceil_div(n_cols, 256))))),             \
+                             256, 0, st>>>(                                                             \
         (const TI*)M, ldm, rows, n_rows, cols, n_cols, (TO*)out, ldo);                               \
   }
   if (transpose) L1F_REQUIRE(ceil_div(n_rows, 32) <= 65535, L1F_ERR_UNSUPPORTED, "gather: too many rows");
