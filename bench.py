@@ -200,7 +200,11 @@ def run_reference(args):
     block = philox_gen.block(0, cfgd["kind"], m, n, r, cfgd["rho_s"], cfgd["magnitude"], ri, ci, x=x, y=y)
     rec = seed_pcp.recover(block.astype(np.float64), tol=TOL)
     seed_np = {"row_idx": ri, "col_idx": ci, "u": rec[0], "sigma": rec[1], "v": rec[2]}
-    units = args.cpu_sample_units or default_cpu_units(cfgd)
+    # per-step sample: whole waves of the reference's 64-unit chunks on every host thread (so the
+    # extrapolation sees the full run's parallelism), and about a minute of CPU time in total
+    wave = 64 * threads
+    units = args.cpu_sample_units or wave * max(1, round(default_cpu_units(cfgd) * 5 / max(1, args.steps + args.warmup)
+                                                        / wave))
     times = []
     for i in range(args.warmup + args.steps):
         out = cpu_sample(cfgd, seed_np, m, n, units, threads)
@@ -324,7 +328,8 @@ def run_ours(args):
         seed_np = {"row_idx": seed.row_idx, "col_idx": seed.col_idx, "u": seed.u.cpu().numpy(),
                    "sigma": seed.sigma.cpu().numpy(), "v": seed.v.cpu().numpy()}
         threads = len(os.sched_getaffinity(0))
-        units = args.cpu_sample_units or default_cpu_units(cfgd)
+        wave = 64 * threads  # whole waves of 64-unit chunks on every host thread
+        units = args.cpu_sample_units or wave * max(1, round(default_cpu_units(cfgd) / wave))
         out = cpu_sample(cfgd, seed_np, m, n, units, threads)
         cpu = {"value": out["value"], "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{out['units_sampled']} ADM units (numpy oracle, 64-unit chunks on {threads} threads) + "
