@@ -259,3 +259,28 @@ def test_svd_gram_matches_gesvd_on_low_rank(m, n, r):
         assert np.abs(b.T @ b - np.eye(r)).max() <= 1e-10
     rec = (u2[:, :r] * torch.from_numpy(s2[:r]).cuda()) @ v2[:, :r].T
     assert torch.linalg.norm(rec - t) <= 1e-11 * torch.linalg.norm(t)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_filter_and_full_adm_agree(seed):
+    """Acceptance property of the reference (test_acceptance.py:69-81): l1 filtering and the full
+    ADM recover the same low-rank part (relative deviation <= 1e-4), both on the device."""
+    gt = l1pcp.generate(l1pcp.SynthSpec(m=500, n=500, rho_r=0.01, rho_s=0.01, rng_seed=seed))
+    filt = l1pcp.estimate_rank_and_solve(gt.m_obs, l1pcp.FilterConfig(rank_hint=5, rng_seed=seed))
+    adm = l1pcp.solve_pcp(gt.m_obs)
+    dev = np.linalg.norm(filt.l - adm.l) / np.linalg.norm(adm.l)
+    assert dev <= 1e-4, dev
+
+
+def test_filter_and_full_adm_agree_large_fp32():
+    """Same agreement at 2000^2, rank 20, on fp32 device tensors (the full ADM's SVT runs on the
+    device through the Gram eigendecomposition)."""
+    mt, l0, _, _ = engine.generate_matrix(2000, 2000, 20, 0.05, 500.0, seed=4, want_l0=True)
+    filt = l1pcp.estimate_rank_and_solve(mt, l1pcp.FilterConfig(rank_hint=20, rng_seed=0,
+                                                                adm=l1pcp.AdmConfig(tol=1e-7)))
+    adm = l1pcp.solve_pcp(mt.double(), l1pcp.AdmConfig(tol=1e-7))
+    lf, la = filt.l.double(), adm.l.double()
+    dev = float(torch.linalg.norm(lf - la) / torch.linalg.norm(la))
+    err = float(torch.linalg.norm(lf - l0.double()) / torch.linalg.norm(l0.double()))
+    print(f"2000^2 r=20: filter vs ADM {dev:.2e}, filter vs L0 {err:.2e}")
+    assert dev <= 1e-4 and err <= 1e-4
