@@ -51,6 +51,8 @@ def as_device(a, keep_f32=True):
             t = t.cuda()
         return t.contiguous(), False
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if not arr.flags.writeable:  # e.g. np.frombuffer from a file read: torch needs a writable array
+        arr = arr.copy()
     return torch.from_numpy(arr).cuda(), True
 
 
