@@ -85,3 +85,23 @@ def test_synth_same_seed_identical_and_checkerboard(tmp_path, capsys):
     for suffix in ("_clean.pgm", "_corrupted.pgm", "_clean.dmat", "_corrupted.dmat", "_s0.dmat"):
         assert (tmp_path / f"cb{suffix}").exists()
     capsys.readouterr()
+
+
+def test_bench_suite_reports(tmp_path, capsys):
+    out_csv, out_json = tmp_path / "r.csv", tmp_path / "r.json"
+    rc = main(["bench", "--suite", "size-sweep", "--scale", "0.5", "--methods", "l1filter", "adm",
+               "--out-csv", str(out_csv), "--out-json", str(out_json)])
+    assert rc == 0
+    rep = json.loads(out_json.read_text())
+    assert rep["suite"] == "size-sweep" and rep["records"]
+    assert all(not r["error"] for r in rep["records"])
+    assert all(r["rel_err"] <= 1e-3 for r in rep["records"])
+    assert set(rep["summary"]["exponents"]) == {"l1filter", "adm"}
+    assert out_csv.read_text().splitlines()[0].startswith("method,m,n,r")
+    summary = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert summary["records"] == len(rep["records"])
+
+
+def test_parser_rejects_unknown_suite():
+    with pytest.raises(SystemExit):
+        main(["bench", "--suite", "nope"])
