@@ -75,7 +75,7 @@ struct Group {
   float ring_sc[RING];
   long long ring_u[RING];
   long long head, tail, pf_from, pf_to;
-  alignas(8) unsigned long long bar_p, bar_r, bar_a, bar_c;
+  alignas(8) unsigned long long bar_p, bar_q, bar_r, bar_a, bar_c;
   uint32_t fmask;
   uint32_t zmask[2];  // TA: by pass parity, slots whose z_it is 0 (fresh or empty)
 };
@@ -281,6 +281,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   if (tid == 0) {
     for (int g = 0; g < NG; ++g) {
       mbar_init(&groups[g].bar_p, 1);
+      mbar_init(&groups[g].bar_q, 1);
       mbar_init(&groups[g].bar_r, 1);
       mbar_init(&groups[g].bar_a, 1);
       mbar_init(&groups[g].bar_c, 1);
@@ -361,7 +362,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     }
   };
   auto install_unit = [&](int slot, long long u, float sc, int src) {
-    const float b0 = P.beta0 > 0 ? (float)P.beta0 : 1.f / sc;
+    const float b0 = P.beta0 > 0 ? (float)P.beta0 : __frcp_rn(sc);  // correctly rounded 1 / sc
     G.unit[slot] = (int)u;
     G.state[slot] = 1;
     G.it[slot] = 0;
@@ -369,7 +370,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     G.src[slot] = src;
     G.beta_cur[slot] = b0;
     G.beta_next[slot] = b0;
-    G.inv_next[slot] = 1.f / b0;
+    G.inv_next[slot] = __frcp_rn(b0);
     G.beta_max[slot] = P.beta_max > 0 ? (float)P.beta_max : 1e7f * b0;
     G.thresh[slot] = tol * sc;
     G.prev_res[slot] = Limits<float>::inf();
@@ -446,7 +447,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
                      ID_A32 = idesc_bf16(128, 32, 0, 1);
   constexpr uint32_t ID_C96 = idesc_bf16(128, 96, 1, 1), ID_C64 = idesc_bf16(128, 64, 1, 1),
                      ID_C32 = idesc_bf16(128, 32, 1, 1);
-  const uint32_t bar_p = umma::saddr(&G.bar_p), bar_r = umma::saddr(&G.bar_r);
+  const uint32_t bar_p = umma::saddr(&G.bar_p), bar_q = umma::saddr(&G.bar_q), bar_r = umma::saddr(&G.bar_r);
 
   uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
   const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0, group 0
@@ -578,23 +579,81 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     prefetch();  // ring entries claimed by the last decision were consumed by load_slot
     float* rall_p = rall + (size_t)par * C * TS;
     if (C > 1 && gtid == 0) {
-      mbar_arm(&G.bar_p, (uint32_t)((C - 1) * (vmine * TS * 4 + TS * 4)));
+      mbar_arm(&G.bar_p, (uint32_t)((C - 1) * vmine * TS * 4));
+      mbar_arm(&G.bar_q, (uint32_t)((C - 1) * TS * 4));
       uint32_t br = 0;
       for (int c = 0; c < C; ++c)
         if (c != crank) br += (uint32_t)max(0, min(rs, KP - c * rs)) * 192u;
       mbar_arm(&G.bar_r, br);
     }
+    unsigned fmask = 0;  // warp 0: slots that finished at this pass (decision part 1)
+    const bool pdec = prof != nullptr && blockIdx.x == 0 && tid == 0;
     if (gw == 0) {  // CTA-local max|r| per slot -> every CTA (round 1)
       const float m = fmaxf(fmaxf(rpart[lane], rpart[TS + lane]), fmaxf(rpart[2 * TS + lane], rpart[3 * TS + lane]));
       rall_p[crank * TS + lane] = m;
       __syncwarp();
-      if (C > 1)
+      if (C > 1) {
         for (int idx = lane; idx < (C - 1) * (TS / 4); idx += 32) {
           const int d = idx / (TS / 4), ch = idx - d * (TS / 4);
           const int peer = d < crank ? d : d + 1;
           const float* src = rall_p + crank * TS + 4 * ch;
-          st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar_p, peer));
+          st_async16(peer_addr(umma::saddr(src), peer), src, peer_addr(bar_q, peer));
         }
+        mbar_wait(&G.bar_q, ph_x);
+      }
+      // ========== decision part 1 (l1reg.py:100-128) from the global max|r_it|, while the phase-c
+      // MMAs run: stop tests, outputs of finished units (iters, residual, status, z slice), beta schedule
+      const long long tdec0 = pdec ? clock64() : 0;
+      const int slot = lane;
+      bool fin = false;
+      float r = 0.f;
+      for (int c = 0; c < C; ++c) r = fmaxf(r, rall_p[c * TS + slot]);
+      if (G.state[slot] == 1) {
+        if (G.it[slot] > 0) {
+          const float prev = G.prev_res[slot];
+          // |r - prev| / max(r, tiny) < 1e-12 (l1reg.py:103-105): in FP32 a nonzero relative change
+          // is at least ~6e-8, so the test is exactly r == prev
+          static_assert(kStallEps < 1e-8f, "stall test relies on eps below the FP32 resolution");
+          G.stalled[slot] = (r == prev) ? G.stalled[slot] + 1 : 0;
+          G.prev_res[slot] = r;
+          uint8_t code = 0xFF;
+          if (r <= G.thresh[slot]) code = L1F_UNIT_OK;
+          else if (G.stalled[slot] >= kStallIters) code = L1F_UNIT_STALLED;
+          else if (G.it[slot] >= P.max_iter) code = L1F_UNIT_MAXITER;
+          if (code != 0xFF) {
+            fin = true;
+            if (crank == 0) {
+              const int64_t u = G.unit[slot];
+              if (iters) iters[u] = G.it[slot];
+              if (res_out) res_out[u] = r;
+              if (status) status[u] = code;
+            }
+          }
+        }
+        if (!fin) {
+          G.it[slot] += 1;
+          const float bc = G.beta_next[slot];
+          G.beta_cur[slot] = bc;
+          float bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
+          if (bn > G.beta_max[slot]) bn = G.beta_max[slot];
+          G.beta_next[slot] = bn;
+          G.inv_next[slot] = __frcp_rn(bn);
+        }
+      }
+      fmask = __ballot_sync(0xffffffffu, fin);
+      const long long tdec1 = pdec ? clock64() : 0;
+      const float* zsp = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
+      for (unsigned mm = fmask; mm; mm &= mm - 1) {  // my slice of z_it of every finished unit
+        const int sl = __ffs(mm) - 1;
+        const int64_t u = G.unit[sl];
+        for (int row = lane; row < vmine; row += 32)
+          if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zsp[row * TS + 4 * ((sl >> 2) ^ (row & 7)) + (sl & 3)];
+      }
+      if (pdec) {
+        const long long tdec2 = clock64();
+        prof[11] += tdec1 - tdec0;
+        prof[12] += tdec2 - tdec1;
+      }
     }
     mbar_wait(&G.bar_c, ph_c);
     ph_c ^= 1;
@@ -647,50 +706,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     float* zs_cur = zsl + (size_t)par * rs * TS;         // z_{it+1} slice (this pass)
     float* zs_prev = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
     if (gw == 0) {
-      // ========== decision (l1reg.py:100-128) from the global max|r_it|; outputs of finished units
-      const int slot = lane;
-      bool fin = false;
-      float r = 0.f;
-      for (int c = 0; c < C; ++c) r = fmaxf(r, rall_p[c * TS + slot]);
-      if (G.state[slot] == 1) {
-        if (G.it[slot] > 0) {
-          const float prev = G.prev_res[slot];
-          const float rel = fabsf(r - prev) / fmaxf(r, Limits<float>::tiny());
-          G.stalled[slot] = (rel < kStallEps) ? G.stalled[slot] + 1 : 0;
-          G.prev_res[slot] = r;
-          uint8_t code = 0xFF;
-          if (r <= G.thresh[slot]) code = L1F_UNIT_OK;
-          else if (G.stalled[slot] >= kStallIters) code = L1F_UNIT_STALLED;
-          else if (G.it[slot] >= P.max_iter) code = L1F_UNIT_MAXITER;
-          if (code != 0xFF) {
-            fin = true;
-            if (crank == 0) {
-              const int64_t u = G.unit[slot];
-              if (iters) iters[u] = G.it[slot];
-              if (res_out) res_out[u] = r;
-              if (status) status[u] = code;
-            }
-          }
-        }
-        if (!fin) {
-          G.it[slot] += 1;
-          const float bc = G.beta_next[slot];
-          G.beta_cur[slot] = bc;
-          float bn = rho * bc;  // beta = min(rho * beta, beta_max), l1reg.py:128
-          if (bn > G.beta_max[slot]) bn = G.beta_max[slot];
-          G.beta_next[slot] = bn;
-          G.inv_next[slot] = 1.f / bn;
-        }
-      }
-      const unsigned fmask = __ballot_sync(0xffffffffu, fin);
-      for (unsigned mm = fmask; mm; mm &= mm - 1) {  // my slice of z_it of every finished unit
-        const int sl = __ffs(mm) - 1;
-        const int64_t u = G.unit[sl];
-        for (int row = lane; row < vmine; row += 32)
-          if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zs_prev[row * TS + 4 * ((sl >> 2) ^ (row & 7)) + (sl & 3)];
-      }
-      __syncwarp();
+      // ========== decision part 2 (round 2's shadow): refill claims, next pass's parameters
+      const long long tdec0 = pdec ? clock64() : 0;
       if (lane == 0) {
+        cp_async_wait_all();  // ring entries prefetched at the top of this pass (ring_sc)
         for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
         G.pf_from = G.tail > G.head ? G.tail : G.head;
         G.pf_to = G.head + RING;
@@ -699,6 +718,11 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       }
       __syncwarp();
       publish(lane);
+      if (pdec) {
+        const long long tdec3 = clock64();
+        prof[10] += tdec3 - tdec0;
+        prof[14] += __popc(fmask);
+      }
       if constexpr (TA) {
         const unsigned zm = __ballot_sync(0xffffffffu, !(G.state[lane] == 1) || G.it[lane] == 0);
         if (lane == 0) G.zmask[par ^ 1] = zm;
@@ -900,6 +924,9 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
       fprintf(stderr, "[tc prof] KP=%d NG=%d NA=%d C=%d clusters=%d smem=%u", KP, NG, NA, C, nclusters, Lo.total);
       for (int i = 0; i < 10; ++i)
         fprintf(stderr, " %s=%.0f", names[i], i ? (double)prof[i] / (double)prof[0] : (double)prof[0]);
+      fprintf(stderr, " decision under phase c (warp0): logic %.0f, z out %.0f; claims+publish in round 2 %.0f; finished/pass %.2f",
+              (double)prof[11] / (double)prof[0], (double)prof[12] / (double)prof[0], (double)prof[10] / (double)prof[0],
+              (double)prof[14] / (double)prof[0]);
       fprintf(stderr, "\n");
       memset(prof, 0, 16 * sizeof(long long));
     }
