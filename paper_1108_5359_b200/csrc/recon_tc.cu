@@ -1,24 +1,27 @@
 // Tensor-core reconstruction L = Af Bf^T, S = M - L (K4 for k > 16) on tcgen05.
 //
 // Reference: nystrom_complete + assemble + s = m - l (pkg/src/l1pcp/l1filter.py:137-167,253) in the
-// unified rank-k form L[i][j] = Af[i] . Bf[j] (see l1f_build_factors).  FP32 accuracy from TF32
-// tensor cores by the 3-pass split: x = hi + lo with hi = x with the low 13 mantissa bits cleared
-// (exact in TF32) and lo = x - hi, and L = Ah Bh^T + Ah Bl^T + Al Bh^T accumulated in FP32 in
-// TMEM (error ~2^-22 relative per product; the parity gate is 1e-4).
+// unified rank-k form L[i][j] = Af[i] . Bf[j] (see l1f_build_factors).  FP32 accuracy from FP16
+// tensor cores by a two-piece split: every factor row is scaled by a power of two 2^e (max |x| 2^e
+// in [2^13, 2^14)), and x 2^e = h + l with h = fp16(x 2^e) and l = fp16(x 2^e - h), 22 significant
+// bits in all.  L = (Ah Bh^T + Ah Bl^T + Al Bh^T) 2^-ea 2^-eb is accumulated in FP32 in TMEM (the
+// dropped Al Bl^T term is ~2^-22 relative; the parity gate is 1e-4); the power-of-two scales are
+// exact.  Same accuracy class as 3xTF32 at the FP16 rate (twice TF32) and half the operand bytes
+// per K, so a K chunk of 32 costs what 16 did in TF32: half the MMA time and half the operand-
+// pipeline round trips per tile.  The split runs once per call (split_factor_kernel).
 //
-// Persistent CTAs (one per SM), 16 warps:
-//   warp 0      TMA producer: fp32 chunks of Af (128 x 32) and Bf (128 x 32), SWIZZLE_128B, K-major
-//   warp 1      TMEM allocation + MMA issuer (one thread): 12 tcgen05.mma.kind::tf32 per chunk
-//   warps 4-7   splitters: lo = x - hi into a second buffer (same swizzled layout); hi is the fp32
-//               word itself (kind::tf32 ignores its low 13 mantissa bits)
-//   warps 8-15  epilogue: tcgen05.ld (row x 16 columns per thread), M via TMA, S = M - L,
+// Persistent CTAs (one per SM), 12 warps (2, 3 idle):
+//   warp 0      TMA producer: fp16 chunks Ah, Al (128 x 32) and Bh, Bl (128 x 32), SWIZZLE_64B, K-major
+//   warp 1      TMEM allocation + MMA issuer (one thread): 6 tcgen05.mma.kind::f16 per chunk
+//   warps 4-11  epilogue: tcgen05.ld (row x 16 columns per thread), scales, M via TMA, S = M - L,
 //               L and S staged in shared memory and written with TMA stores
 // Two 128x128 FP32 accumulators in TMEM (256 columns) overlap the MMA of tile t+1 with the
-// epilogue of tile t; four operand stages overlap loads, splits and MMAs.  Edges are handled by TMA
-// (zero fill on load, clipping on store).  12 B of DRAM traffic per output entry.
+// epilogue of tile t; four operand stages overlap loads and MMAs.  Edges are handled by TMA (zero
+// fill on load, clipping on store).  12 B of DRAM traffic per output entry.
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -27,33 +30,36 @@
 namespace l1f {
 namespace rtc {
 
-constexpr int BM = 128, BN = 128, BK = 16;      // K chunk of 16 fp32 = 64-byte rows (SWIZZLE_64B)
+constexpr int BM = 128, BN = 128, BK = 32;      // K chunk of 32 fp16 = 64-byte rows (SWIZZLE_64B)
 #ifndef L1F_RTC_STAGES
 #define L1F_RTC_STAGES 4
 #endif
 #ifndef L1F_RTC_NMB
 #define L1F_RTC_NMB 4
 #endif
-constexpr int STAGES = L1F_RTC_STAGES;          // operand stages (TMA -> lo split -> MMA)
+constexpr int STAGES = L1F_RTC_STAGES;          // operand stages (TMA -> MMA)
 constexpr int NMB = L1F_RTC_NMB;                // M buffers
 constexpr int MPF = NMB - 2;                    // M prefetch distance (chunks)
-constexpr int NTHREADS = 512;
-constexpr int EPI = 256;  // epilogue threads: warps 8-15, two per TMEM lane quarter (16 columns each)
-constexpr uint32_t OP_BYTES = BM * BK * 4;      // 8 KB: one 128 x 16 fp32 operand box
+constexpr int NTHREADS = 384;
+constexpr int EPI0 = 4;   // first epilogue warp
+constexpr int EPI = 256;  // epilogue threads: warps 4-11, two per TMEM lane quarter (16 columns each)
+constexpr uint32_t OP_BYTES = BM * BK * 2;      // 8 KB: one 128 x 32 fp16 operand box
 constexpr uint32_t CHUNK_BYTES = BM * 32 * 4;   // 16 KB: one 128 x 32 fp32 epilogue box (SWIZZLE_128B)
 constexpr int GROUP = 8;                        // row tiles per raster group (L2 reuse of Bf)
+constexpr int kScaleExp = 14;                   // max |x| 2^e in [2^13, 2^14)
 
 struct Smem {
   // every buffer is a multiple of 1024 bytes (swizzle atoms)
-  uint8_t a_raw[STAGES][OP_BYTES];
-  uint8_t b_raw[STAGES][OP_BYTES];
+  uint8_t a_hi[STAGES][OP_BYTES];
   uint8_t a_lo[STAGES][OP_BYTES];
+  uint8_t b_hi[STAGES][OP_BYTES];
   uint8_t b_lo[STAGES][OP_BYTES];
   uint8_t mbuf[NMB][CHUNK_BYTES];  // M chunk, overwritten in place by S before its TMA store
   uint8_t lbuf[2][CHUNK_BYTES];
-  unsigned long long full[STAGES], conv[STAGES], empty[STAGES];
+  unsigned long long full[STAGES], empty[STAGES];
   unsigned long long tfull[2], tempty[2];
   unsigned long long mfull[NMB];
+  float colscale[2][BN];  // 2^-eb of the tile's columns, by tile parity
   uint32_t tmem_base;
   double red[2][8];
 };
@@ -100,12 +106,12 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
   return d;
 }
-// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = 128
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+// instruction descriptor: D f32, A/B f16, K-major both, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
                ::"r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(acc) : "memory");
 }
 __device__ __forceinline__ void mma_commit(void* bar) {
@@ -125,16 +131,18 @@ struct Sched {
 };
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+recon_tc_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                 const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmL,
-                const __grid_constant__ CUtensorMap tmS, int kchunks, Sched sch, int has_m, int has_l, int has_s,
-                double* __restrict__ part) {
+                const __grid_constant__ CUtensorMap tmS, const float* __restrict__ inv_a,
+                const float* __restrict__ inv_b, int64_t m, int64_t n, int kchunks, Sched sch, int has_m, int has_l,
+                int has_s, double* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.conv[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], EPI); }
     for (int b = 0; b < NMB; ++b) mbar_init(&sm.mfull[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -158,9 +166,11 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int kc = 0; kc < kchunks; ++kc, ++it) {
           const int s = it % STAGES, ph = (it / STAGES) & 1;
           mbar_wait(&sm.empty[s], ph ^ 1);
-          mbar_expect_arrive(&sm.full[s], 2 * OP_BYTES);
-          tma_load(sm.a_raw[s], &tmA, kc * BK, tm * BM, &sm.full[s]);
-          tma_load(sm.b_raw[s], &tmB, kc * BK, tn * BN, &sm.full[s]);
+          mbar_expect_arrive(&sm.full[s], 4 * OP_BYTES);
+          tma_load(sm.a_hi[s], &tmAh, kc * BK, tm * BM, &sm.full[s]);
+          tma_load(sm.b_hi[s], &tmBh, kc * BK, tn * BN, &sm.full[s]);
+          tma_load(sm.a_lo[s], &tmAl, kc * BK, tm * BM, &sm.full[s]);
+          tma_load(sm.b_lo[s], &tmBl, kc * BK, tn * BN, &sm.full[s]);
         }
       }
     }
@@ -174,16 +184,16 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint32_t d = tmem + (uint32_t)(acc * BN);
       for (int kc = 0; kc < kchunks; ++kc, ++it) {
         const int s = it % STAGES, ph = (it / STAGES) & 1;
-        mbar_wait(&sm.conv[s], ph);
+        mbar_wait(&sm.full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
-          const uint32_t ah = sa(sm.a_raw[s]), bh = sa(sm.b_raw[s]), al = sa(sm.a_lo[s]), bl = sa(sm.b_lo[s]);
+          const uint32_t ah = sa(sm.a_hi[s]), bh = sa(sm.b_hi[s]), al = sa(sm.a_lo[s]), bl = sa(sm.b_lo[s]);
 #pragma unroll
-          for (int j = 0; j < BK / 8; ++j) {
-            const uint32_t off = 32u * j;  // 8 tf32 = 32 bytes along K inside the 64-byte swizzle atom
-            mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), (kc | j) ? 1u : 0u);
-            mma_tf32(d, smem_desc(ah + off), smem_desc(bl + off), 1u);
-            mma_tf32(d, smem_desc(al + off), smem_desc(bh + off), 1u);
+          for (int j = 0; j < BK / 16; ++j) {
+            const uint32_t off = 32u * j;  // 16 fp16 = 32 bytes along K inside the 64-byte swizzle atom
+            mma_f16(d, smem_desc(ah + off), smem_desc(bh + off), (kc | j) ? 1u : 0u);
+            mma_f16(d, smem_desc(ah + off), smem_desc(bl + off), 1u);
+            mma_f16(d, smem_desc(al + off), smem_desc(bh + off), 1u);
           }
           mma_commit(&sm.empty[s]);                         // stage free when these MMAs retire
           if (kc == kchunks - 1) mma_commit(&sm.tfull[acc]);  // accumulator ready
@@ -191,42 +201,11 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         __syncwarp();
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ================= hi / lo split (128 threads)
-    const int ct = threadIdx.x - 128;
-    int it = 0;
-    for (int t = blockIdx.x; t < sch.ntiles; t += gridDim.x) {
-      for (int kc = 0; kc < kchunks; ++kc, ++it) {
-        const int s = it % STAGES, ph = (it / STAGES) & 1;
-        mbar_wait(&sm.full[s], ph);
-        uint4* ar = reinterpret_cast<uint4*>(sm.a_raw[s]);
-        uint4* br = reinterpret_cast<uint4*>(sm.b_raw[s]);
-        float4* alo = reinterpret_cast<float4*>(sm.a_lo[s]);
-        float4* blo = reinterpret_cast<float4*>(sm.b_lo[s]);
-#pragma unroll 4
-        for (int e = ct; e < (int)(OP_BYTES / 16); e += 128) {
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            uint4* raw = w ? br : ar;
-            float4* lo = w ? blo : alo;
-            uint4 x = raw[e];
-            uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
-            lo[e] = make_float4(__uint_as_float(x.x) - __uint_as_float(h.x), __uint_as_float(x.y) - __uint_as_float(h.y),
-                                __uint_as_float(x.z) - __uint_as_float(h.z), __uint_as_float(x.w) - __uint_as_float(h.w));
-            // hi stays in place: the tensor core reads TF32 from the fp32 word and ignores the low
-            // 13 mantissa bits, i.e. uses exactly h
-          }
-        }
-        fence_async_smem();
-        named_bar(2, 128);
-        if (ct == 0) mbar_arrive(&sm.conv[s]);
-      }
-    }
-  } else if (warp >= 8) {
-    // ================= epilogue (128 threads, TMEM lane quarter = warp - 8)
-    const int ew = warp - 8, q = ew & 3, half = ew >> 2;
+  } else if (warp >= EPI0) {
+    // ================= epilogue (256 threads, TMEM lane quarter = warp % 4)
+    const int ew = warp - EPI0, q = warp & 3, half = ew >> 2;
     const int row = 32 * q + lane;  // row of the tile owned by this thread (columns half * 16 .. + 16)
-    const bool leader = threadIdx.x == 256;
+    const bool leader = threadIdx.x == 32 * EPI0;
     double r2 = 0.0, m2 = 0.0;
     int ti = 0, g = 0;
     // chunk g -> (tile, column chunk); prefetch M of chunk g+1 while g is processed
@@ -240,7 +219,7 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       y = tm * BM;
       return true;
     };
-    if (leader && has_m) {  // M of the first four chunks
+    if (leader && has_m) {  // M of the first chunks
       for (int gg = 0; gg < MPF; ++gg) {
         int x, y;
         if (chunk_coords(gg, x, y)) {
@@ -253,6 +232,13 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int tm, tn;
       sch.tile(t, tm, tn);
       const int acc = ti & 1, aph = (ti >> 1) & 1;
+      const int64_t gi = (int64_t)tm * BM + row;
+      const float sca = gi < m ? inv_a[gi] : 0.f;  // 2^-ea of this row
+      {
+        const int et = threadIdx.x - 32 * EPI0;
+        const int64_t gj = (int64_t)tn * BN + et;
+        if (et < BN) sm.colscale[ti & 1][et] = gj < n ? inv_b[gj] : 0.f;  // read after the next named barrier
+      }
       mbar_wait(&sm.tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       for (int cc = 0; cc < BN / 32; ++cc, ++g) {
@@ -292,8 +278,11 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int j = 4 * half + jj, p = j ^ (row & 7);
-          const float4 l4 = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
-                                        __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+          const float4 c4 = *reinterpret_cast<const float4*>(&sm.colscale[ti & 1][cc * 32 + 4 * j]);
+          const float4 l4 = make_float4(__uint_as_float(v[4 * jj]) * sca * c4.x,
+                                        __uint_as_float(v[4 * jj + 1]) * sca * c4.y,
+                                        __uint_as_float(v[4 * jj + 2]) * sca * c4.z,
+                                        __uint_as_float(v[4 * jj + 3]) * sca * c4.w);
           if (has_l) lrow[p] = l4;
           if (has_m) {
             const float4 m4 = mrow[p];
@@ -331,14 +320,28 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-// zero-padded copy of a rows x k factor to rows x kp (TMA needs a 16-byte row pitch; kp % 16 == 0)
-__global__ void pad_factor_kernel(const float* __restrict__ src, int64_t rows, int k, int64_t lds, int kp,
-                                  float* __restrict__ dst) {
-  const int64_t total = rows * (int64_t)kp;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / kp;
-    const int t = (int)(e - r * kp);
-    dst[e] = t < k ? src[r * lds + t] : 0.0f;
+// two-piece FP16 split of a rows x k factor into rows x kp (kp % 32 == 0, zero padded): one warp
+// per row; x 2^e = h + l with max |x| 2^e in [2^13, 2^14), inv[row] = 2^-e (1 for a zero row)
+__global__ void split_factor_kernel(const float* __restrict__ src, int64_t rows, int k, int64_t lds, int kp,
+                                    __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ inv) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const float* x = src + r * lds;
+    float mx = 0.f;
+    for (int t = lane; t < k; t += 32) mx = fmaxf(mx, fabsf(x[t]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int ex = 0;
+    if (mx > 0.f) frexpf(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
+    const int e = mx > 0.f ? kScaleExp - ex : 0;
+    for (int t = lane; t < kp; t += 32) {
+      const float v = t < k ? ldexpf(x[t], e) : 0.f;
+      const __half h = __float2half_rn(v);
+      hi[r * kp + t] = h;
+      lo[r * kp + t] = __float2half_rn(v - __half2float(h));
+    }
+    if (lane == 0) inv[r] = ldexpf(1.f, -e);
   }
 }
 
@@ -364,16 +367,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D fp32 tensor (rows x cols, row pitch ld elements), box_cols x 128 boxes
+// 2D fp32 (or fp16) tensor (rows x cols, row pitch ld elements), box_cols x 128 boxes
 static bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
-                     CUtensorMapSwizzle swz) {
+                     CUtensorMapSwizzle swz, bool f16 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (f16 ? 2 : 4))};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, 128};
   cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+  return fn(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -394,21 +397,28 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
     return L1F_ERR_UNSUPPORTED;
   if (m >= INT32_MAX || n >= INT32_MAX || !encode_fn()) return L1F_ERR_UNSUPPORTED;
   const int kp = (int)ceil_div(k, BK) * BK;
-  float *ap = nullptr, *bp = nullptr;
+  __half *ah = nullptr, *al = nullptr, *bh = nullptr, *bl = nullptr;
+  float *ia = nullptr, *ib = nullptr;
   double* part = nullptr;
   const int grid = num_sms();
-  L1F_CUDA_TRY(cudaMallocAsync(&ap, sizeof(float) * (size_t)m * kp, st));
-  L1F_CUDA_TRY(cudaMallocAsync(&bp, sizeof(float) * (size_t)n * kp, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&ah, sizeof(__half) * (size_t)m * kp * 2, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&bh, sizeof(__half) * (size_t)n * kp * 2, st));
+  const int64_t m4 = ceil_div(m, 4) * 4;  // inv_b 16-byte aligned (float4 loads)
+  L1F_CUDA_TRY(cudaMallocAsync(&ia, sizeof(float) * (size_t)(m4 + n), st));
   L1F_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * 2 * grid, st));
-  pad_factor_kernel<<<grid * 4, 256, 0, st>>>(Af, m, k, ldaf, kp, ap);
-  pad_factor_kernel<<<grid * 4, 256, 0, st>>>(Bf, n, k, ldbf, kp, bp);
-  CUtensorMap tA, tB, tM, tL, tS;
-  const auto W = CU_TENSOR_MAP_SWIZZLE_128B;
-  bool ok = make_map(&tA, ap, m, kp, kp, BK, CU_TENSOR_MAP_SWIZZLE_64B) &&
-            make_map(&tB, bp, n, kp, kp, BK, CU_TENSOR_MAP_SWIZZLE_64B);
-  ok = ok && make_map(&tM, M ? (const void*)M : (const void*)ap, M ? m : 1, M ? n : 32, M ? ldm : 32, 32, W);
-  ok = ok && make_map(&tL, L ? (const void*)L : (const void*)ap, L ? m : 1, L ? n : 32, L ? ldl : 32, 32, W);
-  ok = ok && make_map(&tS, S ? (const void*)S : (const void*)ap, S ? m : 1, S ? n : 32, S ? lds : 32, 32, W);
+  al = ah + (size_t)m * kp;
+  bl = bh + (size_t)n * kp;
+  ib = ia + m4;
+  split_factor_kernel<<<grid * 4, 256, 0, st>>>(Af, m, k, ldaf, kp, ah, al, ia);
+  split_factor_kernel<<<grid * 4, 256, 0, st>>>(Bf, n, k, ldbf, kp, bh, bl, ib);
+  CUtensorMap tAh, tAl, tBh, tBl, tM, tL, tS;
+  const auto W = CU_TENSOR_MAP_SWIZZLE_128B, W64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  bool ok = make_map(&tAh, ah, m, kp, kp, BK, W64, true) && make_map(&tAl, al, m, kp, kp, BK, W64, true) &&
+            make_map(&tBh, bh, n, kp, kp, BK, W64, true) && make_map(&tBl, bl, n, kp, kp, BK, W64, true);
+  const void* dummy = ia;  // any 16-byte aligned device pointer for unused maps
+  ok = ok && make_map(&tM, M ? (const void*)M : dummy, M ? m : 1, M ? n : 32, M ? ldm : 32, 32, W);
+  ok = ok && make_map(&tL, L ? (const void*)L : dummy, L ? m : 1, L ? n : 32, L ? ldl : 32, 32, W);
+  ok = ok && make_map(&tS, S ? (const void*)S : dummy, S ? m : 1, S ? n : 32, S ? lds : 32, 32, W);
   int rc = L1F_OK;
   if (!ok) {
     set_error("reconstruct: cuTensorMapEncodeTiled failed");
@@ -428,8 +438,9 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
     // L1F_RECON_TC_MASK (diagnostics): bit 0 drops M, bit 1 drops L, bit 2 drops S
     const char* mk = getenv("L1F_RECON_TC_MASK");
     const int mask = mk ? atoi(mk) : 0;
-    recon_tc_kernel<<<g, NTHREADS, smem, st>>>(tA, tB, tM, tL, tS, kp / BK, sch, M != nullptr && !(mask & 1),
-                                               L != nullptr && !(mask & 2), S != nullptr && !(mask & 4), part);
+    recon_tc_kernel<<<g, NTHREADS, smem, st>>>(tAh, tAl, tBh, tBl, tM, tL, tS, ia, ib, m, n, kp / BK, sch,
+                                               M != nullptr && !(mask & 1), L != nullptr && !(mask & 2),
+                                               S != nullptr && !(mask & 4), part);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error("reconstruct (tcgen05): launch failed: %s", cudaGetErrorString(e));
@@ -438,8 +449,9 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
       sum_parts_kernel<<<1, 32, 0, st>>>(part, g, resid_sq);
     }
   }
-  cudaFreeAsync(ap, st);
-  cudaFreeAsync(bp, st);
+  cudaFreeAsync(ah, st);
+  cudaFreeAsync(bh, st);
+  cudaFreeAsync(ia, st);
   cudaFreeAsync(part, st);
   return rc;
 }
