@@ -31,23 +31,21 @@ namespace l1f {
 namespace rtc {
 
 constexpr int BM = 128, BN = 128, BK = 32;      // K chunk of 32 fp16 = 64-byte rows (SWIZZLE_64B)
-#ifndef L1F_RTC_STAGES
-#define L1F_RTC_STAGES 4
-#endif
-#ifndef L1F_RTC_NMB
-#define L1F_RTC_NMB 4
-#endif
-constexpr int STAGES = L1F_RTC_STAGES;          // operand stages (TMA -> MMA)
-constexpr int NMB = L1F_RTC_NMB;                // M buffers
-constexpr int MPF = NMB - 2;                    // M prefetch distance (chunks)
+// pipeline depths (template parameters): operand stages (TMA -> MMA) and M buffers (prefetch
+// distance NMB - 2 chunks); measured (tools/run_recon_variants.sh): 3 stages + 6 M buffers for
+// k <= 128, 4 + 4 above (the operand pipeline needs the depth once K grows)
 constexpr int NTHREADS = 384;
 constexpr int EPI0 = 4;   // first epilogue warp
 constexpr int EPI = 256;  // epilogue threads: warps 4-11, two per TMEM lane quarter (16 columns each)
 constexpr uint32_t OP_BYTES = BM * BK * 2;      // 8 KB: one 128 x 32 fp16 operand box
 constexpr uint32_t CHUNK_BYTES = BM * 32 * 4;   // 16 KB: one 128 x 32 fp32 epilogue box (SWIZZLE_128B)
-constexpr int GROUP = 8;                        // row tiles per raster group (L2 reuse of Bf)
+#ifndef L1F_RTC_GROUP
+#define L1F_RTC_GROUP 8
+#endif
+constexpr int GROUP = L1F_RTC_GROUP;            // row tiles per raster group (L2 reuse of Bf)
 constexpr int kScaleExp = 14;                   // max |x| 2^e in [2^13, 2^14)
 
+template <int STAGES, int NMB>
 struct Smem {
   // every buffer is a multiple of 1024 bytes (swizzle atoms)
   uint8_t a_hi[STAGES][OP_BYTES];
@@ -130,6 +128,7 @@ struct Sched {
   }
 };
 
+template <int STAGES, int NMB>
 __global__ void __launch_bounds__(NTHREADS, 1)
 recon_tc_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                 const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
@@ -138,7 +137,9 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant_
                 const float* __restrict__ inv_b, int64_t m, int64_t n, int kchunks, Sched sch, int has_m, int has_l,
                 int has_s, double* __restrict__ part) {
   extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int MPF = NMB - 2;
+  using SmemT = Smem<STAGES, NMB>;
+  SmemT& sm = *reinterpret_cast<SmemT*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
@@ -428,19 +429,22 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
     sch.ntm = (int)ceil_div(m, BM);
     sch.ntn = (int)ceil_div(n, BN);
     sch.ntiles = sch.ntm * sch.ntn;
-    const size_t smem = sizeof(Smem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
     const int g = std::min(grid, sch.ntiles);
     // L1F_RECON_TC_MASK (diagnostics): bit 0 drops M, bit 1 drops L, bit 2 drops S
     const char* mk = getenv("L1F_RECON_TC_MASK");
     const int mask = mk ? atoi(mk) : 0;
-    recon_tc_kernel<<<g, NTHREADS, smem, st>>>(tAh, tAl, tBh, tBl, tM, tL, tS, ia, ib, m, n, kp / BK, sch,
-                                               M != nullptr && !(mask & 1), L != nullptr && !(mask & 2),
-                                               S != nullptr && !(mask & 4), part);
+    static bool attr_set[2] = {false, false};
+    auto run = [&](auto kern, size_t smem, int which) {
+      if (!attr_set[which]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set[which] = true;
+      }
+      kern<<<g, NTHREADS, smem, st>>>(tAh, tAl, tBh, tBl, tM, tL, tS, ia, ib, m, n, kp / BK, sch,
+                                      M != nullptr && !(mask & 1), L != nullptr && !(mask & 2),
+                                      S != nullptr && !(mask & 4), part);
+    };
+    if (kp <= 128) run(recon_tc_kernel<3, 6>, sizeof(Smem<3, 6>) + 1024, 0);
+    else run(recon_tc_kernel<4, 4>, sizeof(Smem<4, 4>) + 1024, 1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error("reconstruct (tcgen05): launch failed: %s", cudaGetErrorString(e));
