@@ -343,7 +343,8 @@ def run_ours(args):
                          f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
                          f"{m}x{n}"}
 
-    launches_per_step = 2 + 2 * 3 + 1 + 2
+    launches_per_step = 2 + 2 * 2 + 1 + 4  # gathers, (unit scale + filter) x 2, factors, split x 2 + recon + sum
+    traffic = ncu_traffic(cfgd)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -357,7 +358,9 @@ def run_ours(args):
                                                    "adm_tc_kernel, tcgen05 bf16x3 (column + row filters)"), "achieved": achieved,
                      "peak": fma_tflops, "unit": "TFLOP/s", "frac": achieved / fma_tflops,
                      "peak_source": "measured FP32 FMA probe (l1f_fma_peak_probe, this run)",
-                     "peak_nominal": 148 * 128 * 2 * 1.965e9 / 1e12, "traffic": None,
+                     "peak_nominal": 148 * 128 * 2 * 1.965e9 / 1e12,
+                     "traffic": traffic.get("filter", {}).get("dram_bytes_per_launch"),
+                     "traffic_source": traffic.get("filter", {}).get("source"),
                      "algorithmic_flops_per_step": flops, "kernel_ms_per_step": t_filter_only},
         "roofline_tensor": tensor_roofline(plan, seed, itc, itr, t_filter_only, peaks),
         "generate": {"bound": "fp32" if r > 16 else "hbm", "ms": gen_ms,
@@ -369,7 +372,9 @@ def run_ours(args):
                              "compute-bound for r > 16; outside the timed step"},
         "roofline_reconstruct": {"bound": "hbm", "achieved": recon_gbs, "peak": hbm, "unit": "GB/s",
                                  "frac": recon_gbs / hbm, "bytes_per_step": recon_bytes, "kernel_ms_per_step": t_recon,
-                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                                 "traffic": traffic.get("reconstruct", {}).get("dram_bytes_per_launch"),
+                                 "traffic_source": traffic.get("reconstruct", {}).get("source")},
         "phases_ms": {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
                       "filters": t_filter_only, "factors": float(np.mean([e[2].elapsed_time(e[3]) for e in ev_all])),
                       "reconstruct": t_recon, "t1_seed_s": t1, "generate_s": t_gen},
@@ -387,6 +392,17 @@ def run_ours(args):
     }
     print(json.dumps(line))
     return 0
+
+
+def ncu_traffic(cfgd):
+    """Per-launch DRAM bytes of the dominant kernels from the committed ncu capture of this
+    workload (profiles/ncu_traffic.json), or {} when none was taken."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(cfgd["name"], {})
+    except (OSError, ValueError, KeyError):
+        return {}
 
 
 def tensor_roofline(plan, seed, itc, itr, t_ms, peaks):
