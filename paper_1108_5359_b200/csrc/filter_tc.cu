@@ -52,7 +52,7 @@ constexpr int TSP = TS;       // fp32 rows of the partial-z inbox
 constexpr int RING = 4;
 constexpr int kStallIters = 20;      // STAGNATION_ITERS, l1reg.py:34
 constexpr float kStallEps = 1e-12f;  // STAGNATION_EPS, l1reg.py:33
-constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, then 96 per phase-c M tile
+constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, then 96 per phase-c M tile (TA: shared)
 
 struct Params {
   int s, k, cluster, rs;
@@ -239,7 +239,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (16 at NG = 2, 8 at NG = 1)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
   constexpr uint32_t ACOLS = TA ? (3u * KP / 2 + 31u) / 32u * 32u : 0u;  // TMEM columns of the TA dictionary
-  constexpr uint32_t GCOLS = TA ? 96u + 32u * MTC : 96u * (1 + MTC);
+  // TA: phase c reuses the phase-a columns (az is read out before phase c is issued), 64 per M tile
+  constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * (1 + MTC);
   static_assert(!TA || NG == 1, "TA runs one slot group");
   static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
   static_assert(ACOLS + NG * GCOLS <= TMEM_COLS, "TMEM columns");
@@ -547,17 +548,14 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll
-      for (int mt = 0; mt < MTC && TA; ++mt) {  // 3 products (a0 v0, a0 v1, a1 v0) of 2-piece A and v'
-        const uint32_t dc = tmem + 96u + 32u * mt;
+      for (int mt = 0; mt < MTC && TA; ++mt) {  // 3 products of 2-piece A and v': a0 [v0 v1] -> 0-63, a1 [v0] -> 32-63
+        const uint32_t dc = tmem + 64u * mt;
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
           const uint32_t aa = a_addr + (uint32_t)(2 * ks) * (KG * 128u) + (uint32_t)(16 * mt) * 128u;
-          const uint32_t vb = v_addr + (uint32_t)(2 * ks) * 1536u;
-          const uint64_t da0 = umma::desc_noswz(aa, KG * 128, 128);
-          mma_bf16(dc, da0, umma::desc_noswz(vb, 1536, 128), ID_C32, ks != 0);
-          mma_bf16(dc, da0, umma::desc_noswz(vb + 4u * 128u, 1536, 128), ID_C32, 1u);
-          mma_bf16(dc, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), umma::desc_noswz(vb, 1536, 128),
-                   ID_C32, 1u);
+          const uint64_t db = umma::desc_noswz(v_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
+          mma_bf16(dc, umma::desc_noswz(aa, KG * 128, 128), db, ID_C64, ks != 0);
+          mma_bf16(dc + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), db, ID_C32, 1u);
         }
       }
 #pragma unroll
@@ -662,11 +660,14 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 #pragma unroll
     for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
       float zp[SPT];
-      if constexpr (TA) {
-        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u + 32u * mt + (uint32_t)slot0;
-        if constexpr (SPT == 16) umma::ld16(tc, zp);
-        else umma::ld8(tc, zp);
+      if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+        float b0[SPT], b1[SPT];
+        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)slot0;
+        if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
+        else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); }
         umma::ld_wait();
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) zp[j] = b1[j] + b0[j];
       } else {
         float b0[SPT], b1[SPT], b2[SPT];
         const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * (1 + mt) + (uint32_t)slot0;
