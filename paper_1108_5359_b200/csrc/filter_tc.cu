@@ -52,7 +52,7 @@ constexpr int TSP = TS;       // fp32 rows of the partial-z inbox
 constexpr int RING = 4;
 constexpr int kStallIters = 20;      // STAGNATION_ITERS, l1reg.py:34
 constexpr float kStallEps = 1e-12f;  // STAGNATION_EPS, l1reg.py:33
-constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, then 96 per phase-c M tile (TA: shared)
+constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, reused by phase c (96 per M tile)
 
 struct Params {
   int s, k, cluster, rs;
@@ -83,12 +83,20 @@ struct Group {
 template <int KP, int NA>
 constexpr uint32_t a_bytes() { return (uint32_t)NA * SL * KP * 2u; }
 
-template <int KP, int NG, int NA>
+template <int KP, int NG, int NA, bool TA>
 Layout make_layout(int C, int rs) {
   Layout L;
   uint32_t o = 0;
-  L.zop = o; o += 3u * KP * TS * 2u;
-  L.vop = o; o += 3u * SL * TS * 2u;
+  // z (phase-a B operand, KP rows) and v (phase-c B operand, SL rows) share one buffer: v is
+  // written in phase b after phase a has consumed z, and z_{it+1} arrives (round 2, local and
+  // from peers) only after every CTA's phase c has consumed v (round 1 follows phase c)
+  // (the TA variant keeps separate buffers: measured 3% faster at cfg5)
+  if (TA) {
+    L.zop = o; o += 3u * KP * TS * 2u;
+    L.vop = o; o += 3u * SL * TS * 2u;
+  } else {
+    L.zop = o; L.vop = o; o += 3u * (uint32_t)(KP > SL ? KP : SL) * TS * 2u;
+  }
   L.zin = o; o += (uint32_t)(C * rs) * TSP * 4u;
   L.zsl = o; o += 2u * (uint32_t)rs * TS * 4u;
   L.ring = o; o += RING * SL * 4u;
@@ -239,8 +247,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (16 at NG = 2, 8 at NG = 1)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
   constexpr uint32_t ACOLS = TA ? (3u * KP / 2 + 31u) / 32u * 32u : 0u;  // TMEM columns of the TA dictionary
-  // TA: phase c reuses the phase-a columns (az is read out before phase c is issued), 64 per M tile
-  constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * (1 + MTC);
+  // phase c reuses the phase-a columns (az is read out before phase c is issued): 96 per M tile
+  // (TA: 64 per M tile)
+  constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * MTC;
   static_assert(!TA || NG == 1, "TA runs one slot group");
   static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
   static_assert(ACOLS + NG * GCOLS <= TMEM_COLS, "TMEM columns");
@@ -331,7 +340,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   Group& G = groups[g];
   unsigned char* gb = smem_raw + Lo.group0 + g * Lo.gstride;
   __nv_bfloat16* zop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.zop);  // [3][KP*TS] phase-a operand
-  __nv_bfloat16* vop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.vop);  // [3][SL*TS] phase-c operand
+  __nv_bfloat16* vop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.vop);  // [3][SL*TS] phase-c operand (= zop)
   float* zin = reinterpret_cast<float*>(gb + Lo.zin);      // [C*rs][TSP] partials of my slice, by sender
   float* zsl = reinterpret_cast<float*>(gb + Lo.zsl);      // [2][rs][TS] reduced slice (pass parity)
   float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RING][SL]
@@ -560,7 +569,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       }
 #pragma unroll
       for (int mt = 0; mt < MTC && !TA; ++mt) {
-        const uint32_t dc = tmem + 96u * (1 + mt);
+        const uint32_t dc = tmem + 96u * mt;
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
           const uint64_t db = umma::desc_noswz(v_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
@@ -670,7 +679,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         for (int j = 0; j < SPT; ++j) zp[j] = b1[j] + b0[j];
       } else {
         float b0[SPT], b1[SPT], b2[SPT];
-        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * (1 + mt) + (uint32_t)slot0;
+        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)slot0;
         if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
         else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
         umma::ld_wait();
@@ -854,10 +863,10 @@ __global__ void unit_scale_kernel(const float* __restrict__ X, Params P, float* 
 
 constexpr uint32_t kSmemLimit = 227u * 1024u - 6144u;  // dynamic budget next to the static Group state
 
-template <int KP, int NG, int NA>
+template <int KP, int NG, int NA, bool TA = false>
 bool fits(int s) {
   const int C = (int)ceil_div(s, SL);
-  return make_layout<KP, NG, NA>(C, (int)ceil_div(KP, C)).total <= kSmemLimit;
+  return make_layout<KP, NG, NA, TA>(C, (int)ceil_div(KP, C)).total <= kSmemLimit;
 }
 
 template <int KP, int NG, int NA, bool TA = false>
@@ -867,7 +876,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
            size_t* need) {
   const int C = (int)ceil_div(s, SL);
   const int rs = (int)ceil_div(KP, C);
-  const Layout Lo = make_layout<KP, NG, NA>(C, rs);
+  const Layout Lo = make_layout<KP, NG, NA, TA>(C, rs);
   const size_t scale_bytes = (sizeof(float) * (size_t)(n_units > 0 ? n_units : 1) + 255) & ~(size_t)255;
   if (query) { *need = scale_bytes; return L1F_OK; }
   auto kern = adm_tc_kernel<KP, NG, NA, TA>;
@@ -980,7 +989,7 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
   }
   // larger k: dictionary for phase a in TMEM (3 pieces), 2 pieces in shared memory for phase c
 #define L1F_TA(KP)                                                                                              \
-  if (fits<KP, 1, 2>(s))                                                                                         \
+  if (fits<KP, 1, 2, true>(s))                                                                                   \
     return launch<KP, 1, 2, true>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E,   \
                                   lde, iters, res, status, workspace, ws_bytes, st, query, need)
   switch ((int)l1f::ceil_div(k, 16) * 16) {
