@@ -47,9 +47,12 @@ namespace tcf {
 
 constexpr int TS = 32;        // unit slots per group (MMA N)
 constexpr int SL = 128;       // dictionary rows per CTA (MMA M of phase a)
-constexpr int NT = 512;       // threads per CTA (NG slot groups of NT / NG threads)
+// threads per CTA: NG slot groups of 4 or 8 warps (NG = 3: 4 warps, 32 slots per thread in phase b)
+__host__ __device__ constexpr int threads_of(int NG) { return NG == 3 ? 384 : 512; }
+// ring of prefetched units per group (NG = 3: 2 entries, the shared-memory budget)
+__host__ __device__ constexpr int ring_of(int NG) { return NG == 3 ? 2 : 4; }
 constexpr int TSP = TS;       // fp32 rows of the partial-z inbox
-constexpr int RING = 4;
+constexpr int RING = 4;      // Group ring arrays (ring_of(NG) <= RING entries used)
 constexpr int kStallIters = 20;      // STAGNATION_ITERS, l1reg.py:34
 constexpr float kStallEps = 1e-12f;  // STAGNATION_EPS, l1reg.py:33
 constexpr uint32_t TMEM_COLS = 512;  // per group: phase a 96 columns, reused by phase c (96 per M tile)
@@ -99,7 +102,7 @@ Layout make_layout(int C, int rs) {
   }
   L.zin = o; o += (uint32_t)(C * rs) * TSP * 4u;
   L.zsl = o; o += 2u * (uint32_t)rs * TS * 4u;
-  L.ring = o; o += RING * SL * 4u;
+  L.ring = o; o += (uint32_t)ring_of(NG) * SL * 4u;
   L.rall = o; o += 2u * (uint32_t)C * TS * 4u;
   L.rpart = o; o += 4u * TS * 4u;
   L.gstride = (o + 127u) & ~127u;
@@ -237,14 +240,17 @@ __device__ __forceinline__ float slot_max(float (&v)[N], int lane) {
 // z = A^T v for orthonormal A, and its fixed point does not depend on the precision of phase c
 // (only phase a defines the model A z whose residual is tested).
 template <int KP, int NG, int NA, bool TA>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(threads_of(NG), 1)
 adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t lda, const float* __restrict__ scale,
               Params P, Layout Lo, float* __restrict__ Z, float* __restrict__ E, int32_t* __restrict__ iters,
               float* __restrict__ res_out, uint8_t* __restrict__ status, long long* __restrict__ prof) {
   constexpr int KG = KP / 8;
+  constexpr int NT = threads_of(NG);
+  constexpr int RNG = ring_of(NG);
   constexpr int GT = NT / NG;              // threads per group
   constexpr int WPG = GT / 32;             // warps per group (4 per TMEM lane quarter at NG = 1)
-  constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (16 at NG = 2, 8 at NG = 1)
+  constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (32 at NG = 3, 16 at NG = 2, 8 at NG = 1)
+  constexpr int BS = SPT > 16 ? 8 : SPT;   // slots per TMEM-load block (bounds the registers)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
   constexpr uint32_t ACOLS = TA ? (3u * KP / 2 + 31u) / 32u * 32u : 0u;  // TMEM columns of the TA dictionary
   // phase c reuses the phase-a columns (az is read out before phase c is issued): 96 per M tile
@@ -343,7 +349,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   __nv_bfloat16* vop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.vop);  // [3][SL*TS] phase-c operand (= zop)
   float* zin = reinterpret_cast<float*>(gb + Lo.zin);      // [C*rs][TSP] partials of my slice, by sender
   float* zsl = reinterpret_cast<float*>(gb + Lo.zsl);      // [2][rs][TS] reduced slice (pass parity)
-  float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RING][SL]
+  float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RNG][SL]
   float* rall = reinterpret_cast<float*>(gb + Lo.rall);    // [2][C][TS] per-CTA slot max|r| (parity)
   float* rpart = reinterpret_cast<float*>(gb + Lo.rpart);  // [4][TS]
   const uint32_t tmem = tmem_base + ACOLS + GCOLS * g;
@@ -359,7 +365,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   auto cand = [&](long long j) -> long long { return (long long)vid + j * (long long)nv; };
   auto prefetch = [&]() {
     for (long long j = G.pf_from; j < G.pf_to; ++j) {
-      const int e = (int)(j % RING);
+      const int e = (int)(j % RNG);
       const long long u = cand(j);
       const bool ok = u < P.n_units;
       for (int r = gtid; r < SL; r += GT)
@@ -388,7 +394,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   auto claim_into = [&](int slot) {
     for (;;) {
       if (G.head < G.tail) {
-        const int e = (int)(G.head % RING);
+        const int e = (int)(G.head % RNG);
         const long long u = G.ring_u[e];
         G.head++;
         if (u >= P.n_units) break;
@@ -424,18 +430,18 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     lr[j] = 0.f;
   };
 
-  if (gtid == 0) { G.head = 0; G.tail = 0; G.pf_from = 0; G.pf_to = RING; }
+  if (gtid == 0) { G.head = 0; G.tail = 0; G.pf_from = 0; G.pf_to = RNG; }
   bar_sync(gbar, GT);
   prefetch();
   cp_async_wait_all();
   bar_sync(gbar, GT);
   if (gtid == 0) {
-    G.tail = RING;
+    G.tail = RNG;
     for (int sl = 0; sl < TS; ++sl) claim_into(sl);
     G.fmask = 0;
     G.zmask[0] = 0xFFFFFFFFu;
     G.pf_from = G.tail;
-    G.pf_to = G.head + RING;
+    G.pf_to = G.head + RNG;
     if (G.pf_to < G.pf_from) G.pf_to = G.pf_from;
   }
   bar_sync(gbar, GT);
@@ -491,62 +497,127 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     ph_a ^= 1;
     umma::fence_after();
     stamp(1);
-    float az[SPT];
-    {  // the three order blocks, summed smallest first
-      float b0[SPT], b1[SPT], b2[SPT];
-      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0;
-      if constexpr (SPT == 16) { umma::ld16(ta, b0); umma::ld16(ta + 32, b1); umma::ld16(ta + 64, b2); }
-      else { umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2); }
-      umma::ld_wait();
-#pragma unroll
-      for (int j = 0; j < SPT; ++j) az[j] = (b2[j] + b1[j]) + b0[j];
-    }
-    {
-      const uint32_t fm = (G.fmask >> slot0) & ((1u << SPT) - 1u);
-      if (fm) {
-#pragma unroll
-        for (int j = 0; j < SPT; ++j)
-          if (fm & (1u << j)) load_slot(j);
+    if constexpr (BS == SPT) {  // one TMEM block per thread (NG <= 2)
+      float az[SPT];
+      {  // the three order blocks, summed smallest first
+        float b0[SPT], b1[SPT], b2[SPT];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)slot0;
+        if constexpr (SPT == 16) { umma::ld16(ta, b0); umma::ld16(ta + 32, b1); umma::ld16(ta + 64, b2); }
+        else { umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2); }
+        umma::ld_wait();
+  #pragma unroll
+        for (int j = 0; j < SPT; ++j) az[j] = (b2[j] + b1[j]) + b0[j];
       }
-    }
+      {
+        const uint32_t fm = (G.fmask >> slot0) & ((1u << SPT) - 1u);
+        if (fm) {
+  #pragma unroll
+          for (int j = 0; j < SPT; ++j)
+            if (fm & (1u << j)) load_slot(j);
+        }
+      }
 
-    // ========== phase b: elementwise ADM update (reformulated residual), v -> bf16 pieces
-    if (E != nullptr && grow < P.s) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
-#pragma unroll
-      for (int j = 0; j < SPT; ++j)
-        if (G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
-    }
-    float rmax[SPT];
-#pragma unroll
-    for (int j = 0; j < SPT; ++j) {
-      const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
-      const float tn = pr.y;
-      const float x = xr[j];
-      const float azv = pr.z != 0.f ? 0.f : az[j];
-      const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
-      rmax[j] = fabsf(r);
-      const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
-      const float yb = y * tn;
-      const float w = (x - azv) + yb;
-      const bool sup = fabsf(w) > tn;
-      const float sgt = w > 0.f ? tn : -tn;
-      lr[j] = sup ? (azv - yb) + sgt : x;
-      if constexpr (TA) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
-      else az[j] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
-      yr[j] = y;
-    }
-    // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
-#pragma unroll
-    for (int hh = 0; hh < SPT / 8; ++hh) {
-      float v8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
-      const size_t off = (size_t)((lrow >> 3) * 12 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
-      split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
-    }
-    {  // per-slot max|r| over this warp's 32 rows
-      const float m = slot_max<SPT>(rmax, lane);
-      if ((lane & (32 / SPT - 1)) == 0) rpart[q * TS + slot0 + lane / (32 / SPT)] = m;
+      // ========== phase b: elementwise ADM update (reformulated residual), v -> bf16 pieces
+      if (E != nullptr && grow < P.s) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
+  #pragma unroll
+        for (int j = 0; j < SPT; ++j)
+          if (G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
+      }
+      float rmax[SPT];
+  #pragma unroll
+      for (int j = 0; j < SPT; ++j) {
+        const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
+        const float tn = pr.y;
+        const float x = xr[j];
+        const float azv = pr.z != 0.f ? 0.f : az[j];
+        const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
+        rmax[j] = fabsf(r);
+        const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
+        const float yb = y * tn;
+        const float w = (x - azv) + yb;
+        const bool sup = fabsf(w) > tn;
+        const float sgt = w > 0.f ? tn : -tn;
+        lr[j] = sup ? (azv - yb) + sgt : x;
+        if constexpr (TA) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
+        else az[j] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
+        yr[j] = y;
+      }
+      // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
+  #pragma unroll
+      for (int hh = 0; hh < SPT / 8; ++hh) {
+        float v8[8];
+  #pragma unroll
+        for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
+        const size_t off = (size_t)((lrow >> 3) * 12 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
+        split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+      }
+      {  // per-slot max|r| over this warp's 32 rows
+        const float m = slot_max<SPT>(rmax, lane);
+        if ((lane & (32 / SPT - 1)) == 0) rpart[q * TS + slot0 + lane / (32 / SPT)] = m;
+      }
+    } else {  // NG = 3: blocks of BS slots
+      {  // refilled slots: their x from the ring (or global), y = 0, l = 0
+        const uint32_t fm = (G.fmask >> slot0) & (uint32_t)((1ull << SPT) - 1ull);
+        if (fm) {
+  #pragma unroll
+          for (int j = 0; j < SPT; ++j)
+            if (fm & (1u << j)) load_slot(j);
+        }
+      }
+
+      // ========== phase b: elementwise ADM update (reformulated residual), v -> bf16 pieces
+      if (E != nullptr && grow < P.s) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
+  #pragma unroll
+        for (int j = 0; j < SPT; ++j)
+          if (G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
+      }
+  #pragma unroll
+      for (int bk = 0; bk < SPT / BS; ++bk) {  // blocks of BS slots (bounds the TMEM-load registers)
+        const int sb = slot0 + BS * bk;
+        float az[BS];
+        {  // the three order blocks, summed smallest first
+          float b0[BS], b1[BS], b2[BS];
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)sb;
+          if constexpr (BS == 16) { umma::ld16(ta, b0); umma::ld16(ta + 32, b1); umma::ld16(ta + 64, b2); }
+          else { umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2); }
+          umma::ld_wait();
+  #pragma unroll
+          for (int j = 0; j < BS; ++j) az[j] = (b2[j] + b1[j]) + b0[j];
+        }
+        float rmax[BS];
+  #pragma unroll
+        for (int i = 0; i < BS; ++i) {
+          const int j = BS * bk + i;
+          const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
+          const float tn = pr.y;
+          const float x = xr[j];
+          const float azv = pr.z != 0.f ? 0.f : az[i];
+          const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
+          rmax[i] = fabsf(r);
+          const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
+          const float yb = y * tn;
+          const float w = (x - azv) + yb;
+          const bool sup = fabsf(w) > tn;
+          const float sgt = w > 0.f ? tn : -tn;
+          lr[j] = sup ? (azv - yb) + sgt : x;
+          if constexpr (TA) az[i] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
+          else az[i] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
+          yr[j] = y;
+        }
+        // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
+  #pragma unroll
+        for (int hh = 0; hh < BS / 8; ++hh) {
+          float v8[8];
+  #pragma unroll
+          for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
+          const size_t off = (size_t)((lrow >> 3) * 12 + sb / 8 + hh) * 64 + (lrow & 7) * 8;
+          split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+        }
+        {  // per-slot max|r| over this warp's 32 rows
+          const float m = slot_max<BS>(rmax, lane);
+          if ((lane & (32 / BS - 1)) == 0) rpart[q * TS + sb + lane / (32 / BS)] = m;
+        }
+      }
     }
     umma::fence_async_smem();
     umma::fence_before();
@@ -666,44 +737,92 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     ph_c ^= 1;
     umma::fence_after();
     stamp(3);
-#pragma unroll
-    for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
-      float zp[SPT];
-      if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
-        float b0[SPT], b1[SPT];
-        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)slot0;
-        if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
-        else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); }
-        umma::ld_wait();
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) zp[j] = b1[j] + b0[j];
-      } else {
-        float b0[SPT], b1[SPT], b2[SPT];
-        const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)slot0;
-        if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
-        else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
-        umma::ld_wait();
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
+    if constexpr (BS == SPT) {
+  #pragma unroll
+      for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
+        float zp[SPT];
+        if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+          float b0[SPT], b1[SPT];
+          const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)slot0;
+          if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
+          else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); }
+          umma::ld_wait();
+  #pragma unroll
+          for (int j = 0; j < SPT; ++j) zp[j] = b1[j] + b0[j];
+        } else {
+          float b0[SPT], b1[SPT], b2[SPT];
+          const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)slot0;
+          if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
+          else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
+          umma::ld_wait();
+  #pragma unroll
+          for (int j = 0; j < SPT; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
+        }
+        const int t = 128 * mt + lrow;
+        if (t < KP) {
+          const int owner = t / rs, row = t - owner * rs;
+          // inbox row zr of the owner; its 16-byte chunks are XOR-swizzled by (zr & 7) so that the
+          // owner's (row, slot-group) sum reads are bank-conflict free
+          const int zr = crank * rs + row;
+          float* drow = zin + (size_t)zr * TSP;
+          if (owner == crank) {
+  #pragma unroll
+            for (int i = 0; i < SPT / 4; ++i)
+              *reinterpret_cast<float4*>(drow + 4 * ((slot0 / 4 + i) ^ (zr & 7))) =
+                  make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
+          } else {
+            const uint32_t prow = peer_addr(umma::saddr(drow), owner), pbar = peer_addr(bar_p, owner);
+  #pragma unroll
+            for (int i = 0; i < SPT / 4; ++i)
+              st_async16v(prow + 16 * ((slot0 / 4 + i) ^ (zr & 7)), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3],
+                          pbar);
+          }
+        }
       }
-      const int t = 128 * mt + lrow;
-      if (t < KP) {
-        const int owner = t / rs, row = t - owner * rs;
+    } else {
+  #pragma unroll
+      for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
+        const int t = 128 * mt + lrow;
+        const int owner = t < KP ? t / rs : crank, row = t - owner * rs;
         // inbox row zr of the owner; its 16-byte chunks are XOR-swizzled by (zr & 7) so that the
         // owner's (row, slot-group) sum reads are bank-conflict free
         const int zr = crank * rs + row;
         float* drow = zin + (size_t)zr * TSP;
-        if (owner == crank) {
-#pragma unroll
-          for (int i = 0; i < SPT / 4; ++i)
-            *reinterpret_cast<float4*>(drow + 4 * ((slot0 / 4 + i) ^ (zr & 7))) =
-                make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
-        } else {
-          const uint32_t prow = peer_addr(umma::saddr(drow), owner), pbar = peer_addr(bar_p, owner);
-#pragma unroll
-          for (int i = 0; i < SPT / 4; ++i)
-            st_async16v(prow + 16 * ((slot0 / 4 + i) ^ (zr & 7)), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3],
-                        pbar);
+  #pragma unroll
+        for (int bk = 0; bk < SPT / BS; ++bk) {
+          const int sb = slot0 + BS * bk;
+          float zp[BS];
+          if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+            float b0[BS], b1[BS];
+            const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)sb;
+            if constexpr (BS == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
+            else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); }
+            umma::ld_wait();
+  #pragma unroll
+            for (int j = 0; j < BS; ++j) zp[j] = b1[j] + b0[j];
+          } else {
+            float b0[BS], b1[BS], b2[BS];
+            const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)sb;
+            if constexpr (BS == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
+            else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
+            umma::ld_wait();
+  #pragma unroll
+            for (int j = 0; j < BS; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
+          }
+          if (t < KP) {
+            if (owner == crank) {
+  #pragma unroll
+              for (int i = 0; i < BS / 4; ++i)
+                *reinterpret_cast<float4*>(drow + 4 * ((sb / 4 + i) ^ (zr & 7))) =
+                    make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
+            } else {
+              const uint32_t prow = peer_addr(umma::saddr(drow), owner), pbar = peer_addr(bar_p, owner);
+  #pragma unroll
+              for (int i = 0; i < BS / 4; ++i)
+                st_async16v(prow + 16 * ((sb / 4 + i) ^ (zr & 7)), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3],
+                            pbar);
+            }
+          }
         }
       }
     }
@@ -722,7 +841,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         cp_async_wait_all();  // ring entries prefetched at the top of this pass (ring_sc)
         for (unsigned mm = fmask; mm; mm &= mm - 1) claim_into(__ffs(mm) - 1);
         G.pf_from = G.tail > G.head ? G.tail : G.head;
-        G.pf_to = G.head + RING;
+        G.pf_to = G.head + RNG;
         G.tail = G.pf_to;
         G.fmask = fmask;
       }
@@ -861,12 +980,13 @@ __global__ void unit_scale_kernel(const float* __restrict__ X, Params P, float* 
   }
 }
 
-constexpr uint32_t kSmemLimit = 227u * 1024u - 6144u;  // dynamic budget next to the static Group state
+// dynamic budget next to the static Group state (~2 KB per group)
+constexpr uint32_t smem_limit(int NG) { return 227u * 1024u - (NG == 3 ? 7168u + 256u : 6144u); }
 
 template <int KP, int NG, int NA, bool TA = false>
 bool fits(int s) {
   const int C = (int)ceil_div(s, SL);
-  return make_layout<KP, NG, NA, TA>(C, (int)ceil_div(KP, C)).total <= kSmemLimit;
+  return make_layout<KP, NG, NA, TA>(C, (int)ceil_div(KP, C)).total <= smem_limit(NG);
 }
 
 template <int KP, int NG, int NA, bool TA = false>
@@ -882,7 +1002,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
   auto kern = adm_tc_kernel<KP, NG, NA, TA>;
   static bool configured = false;
   if (!configured) {
-    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
+    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit(NG)));
     L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
@@ -909,7 +1029,7 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     attr[0].val.clusterDim.x = C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.blockDim = dim3(threads_of(NG), 1, 1);
     cfg.dynamicSmemBytes = Lo.total;
     cfg.stream = st;
     cfg.attrs = attr;
@@ -968,7 +1088,18 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
   if (fits<KP, NG, NA>(s))                                                                                        \
     return launch<KP, NG, NA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde,  \
                               iters, res, status, workspace, ws_bytes, st, query, need)
-  if (k <= 112) {  // two slot groups, dictionary in 3 pieces
+  if (k <= 112) {  // three (else two) slot groups, dictionary in 3 pieces; L1F_TC_NG=2 forces two
+    const char* ng = getenv("L1F_TC_NG");
+    if (!(ng && ng[0] == '2')) {
+      switch ((int)l1f::ceil_div(k, 16) * 16) {
+        case 32: L1F_TC(32, 3, 3); break;
+        case 48: L1F_TC(48, 3, 3); break;
+        case 64: L1F_TC(64, 3, 3); break;
+        case 80: L1F_TC(80, 3, 3); break;
+        case 96: L1F_TC(96, 3, 3); break;
+        case 112: L1F_TC(112, 3, 3); break;
+      }
+    }
     switch ((int)l1f::ceil_div(k, 16) * 16) {
       case 32: L1F_TC(32, 2, 3); break;
       case 48: L1F_TC(48, 2, 3); break;
