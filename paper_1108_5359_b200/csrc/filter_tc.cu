@@ -258,7 +258,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * MTC;
   static_assert(!TA || NG == 1, "TA runs one slot group");
   static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
-  static_assert(ACOLS + NG * GCOLS <= TMEM_COLS, "TMEM columns");
+  // NG = 3: the slots' x live in TMEM (32 columns per group, lane = row), not in registers
+  constexpr bool XT = BS != SPT;
+  constexpr uint32_t XCOLS = XT ? (uint32_t)TS : 0u;
+  static_assert(ACOLS + NG * (GCOLS + XCOLS) <= TMEM_COLS, "TMEM columns");
 
   constexpr size_t A_PIECE = (size_t)SL * KP, Z_PIECE = (size_t)KP * TS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -352,7 +355,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   float* ring_x = reinterpret_cast<float*>(gb + Lo.ring);  // [RNG][SL]
   float* rall = reinterpret_cast<float*>(gb + Lo.rall);    // [2][C][TS] per-CTA slot max|r| (parity)
   float* rpart = reinterpret_cast<float*>(gb + Lo.rpart);  // [4][TS]
-  const uint32_t tmem = tmem_base + ACOLS + GCOLS * g;
+  const uint32_t tmem = tmem_base + ACOLS + (GCOLS + XCOLS) * g;
+  const uint32_t xcol = tmem + GCOLS;  // XT: x of slot s at column xcol + s
   const int vid = cid * NG + g, nv = nclusters * NG;      // units vid, vid + nv, ...
 
   // phase b mapping: TMEM lane quarter q (rows 32q .. 32q+31), slots [SPT h, SPT h + SPT)
@@ -360,7 +364,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   const int lrow = 32 * q + lane;
   const int grow = row_base + lrow;
   const int slot0 = SPT * h;
-  float xr[SPT], yr[SPT], lr[SPT];
+  float xr[XT ? 1 : SPT], yr[SPT], lr[SPT];
 
   auto cand = [&](long long j) -> long long { return (long long)vid + j * (long long)nv; };
   auto prefetch = [&]() {
@@ -425,7 +429,12 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     const int64_t u = live ? G.unit[slot] : 0;
     float x = 0.f;
     if (live && grow < P.s) x = src >= 0 ? ring_x[(size_t)src * SL + lrow] : X[u * P.ldx + grow];
-    xr[j] = x;
+    if constexpr (XT) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+                   ::"r"(xcol + ((uint32_t)(32 * q) << 16) + (uint32_t)(slot0 + j)), "r"(__float_as_uint(x)) : "memory");
+    } else {
+      xr[j] = x;
+    }
     yr[j] = 0.f;
     lr[j] = 0.f;
   };
@@ -448,6 +457,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   if (gw == 0) publish(lane);
 #pragma unroll
   for (int j = 0; j < SPT; ++j) load_slot(j);
+  if constexpr (XT) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   bar_sync(gbar, GT);
   if (gtid == 0) G.tail = G.pf_to;
   prefetch();
@@ -562,24 +572,33 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
           for (int j = 0; j < SPT; ++j)
             if (fm & (1u << j)) load_slot(j);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
 
       // ========== phase b: elementwise ADM update (reformulated residual), v -> bf16 pieces
-      if (E != nullptr && grow < P.s) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
+      if (E != nullptr) {  // e_it = x - l of live, non-fresh slots (numpy API path only)
   #pragma unroll
-        for (int j = 0; j < SPT; ++j)
-          if (G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xr[j] - lr[j];
+        for (int bk = 0; bk < SPT / BS; ++bk) {
+          float xb[BS];
+          umma::ld8(xcol + ((uint32_t)(32 * q) << 16) + (uint32_t)(slot0 + BS * bk), xb);
+          umma::ld_wait();
+  #pragma unroll
+          for (int i = 0; i < BS; ++i) {
+            const int j = BS * bk + i;
+            if (grow < P.s && G.prm[slot0 + j].z == 0.f) E[(int64_t)G.unit[slot0 + j] * P.lde + grow] = xb[i] - lr[j];
+          }
+        }
       }
   #pragma unroll
       for (int bk = 0; bk < SPT / BS; ++bk) {  // blocks of BS slots (bounds the TMEM-load registers)
         const int sb = slot0 + BS * bk;
-        float az[BS];
-        {  // the three order blocks, summed smallest first
+        float az[BS], xb[BS];
+        {  // the three order blocks, summed smallest first; x of the block
           float b0[BS], b1[BS], b2[BS];
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)sb;
-          if constexpr (BS == 16) { umma::ld16(ta, b0); umma::ld16(ta + 32, b1); umma::ld16(ta + 64, b2); }
-          else { umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2); }
+          umma::ld8(ta, b0); umma::ld8(ta + 32, b1); umma::ld8(ta + 64, b2);
+          umma::ld8(xcol + ((uint32_t)(32 * q) << 16) + (uint32_t)sb, xb);
           umma::ld_wait();
   #pragma unroll
           for (int j = 0; j < BS; ++j) az[j] = (b2[j] + b1[j]) + b0[j];
@@ -590,7 +609,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const int j = BS * bk + i;
           const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
           const float tn = pr.y;
-          const float x = xr[j];
+          const float x = xb[i];
           const float azv = pr.z != 0.f ? 0.f : az[i];
           const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
           rmax[i] = fabsf(r);
