@@ -270,6 +270,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   __nv_bfloat16* aop = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [3][SL*KP]
 
   cg::cluster_group cluster = cg::this_cluster();
+  const long long t_entry = clock64();
   const int C = P.cluster;
   const int crank = C > 1 ? (int)cluster.block_rank() : 0;
   const int cid = blockIdx.x / C, nclusters = gridDim.x / C;
@@ -476,6 +477,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   const uint32_t bar_p = umma::saddr(&G.bar_p), bar_q = umma::saddr(&G.bar_q), bar_r = umma::saddr(&G.bar_r);
 
   uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
+  long long npass = 0;
+  if (prof != nullptr && blockIdx.x == 0 && tid == 0) prof[19] = clock64() - t_entry;  // prologue
+  const long long t_loop = clock64();
   const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0, group 0
   long long tp[10];
   auto stamp = [&](int i) { if (pf) tp[i] = clock64(); };
@@ -964,7 +968,14 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       for (int i = 1; i < 10; ++i) prof[i] += tp[order[i]] - tp[order[i - 1]];
       prof[0] += 1;
     }
+    ++npass;
     if (!any) break;
+  }
+  if (prof != nullptr && gtid == 0 && crank == 0) {  // pass-count spread over the groups (tail)
+    atomicMax(reinterpret_cast<unsigned long long*>(&prof[16]), (unsigned long long)npass);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&prof[17]), (unsigned long long)npass);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&prof[18]), 1ull);
+    atomicMax(reinterpret_cast<unsigned long long*>(&prof[20 + g]), (unsigned long long)(clock64() - t_loop));
   }
   umma::fence_before();
   __syncthreads();
@@ -1063,8 +1074,8 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     static long long* prof = nullptr;
     const char* pe = getenv("L1F_TC_PROF");
     if (pe && pe[0] == '1' && !prof) {
-      cudaMallocManaged(&prof, 16 * sizeof(long long));
-      memset(prof, 0, 16 * sizeof(long long));
+      cudaMallocManaged(&prof, 24 * sizeof(long long));
+      memset(prof, 0, 24 * sizeof(long long));
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof);
     if (prof) {
@@ -1076,8 +1087,10 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
       fprintf(stderr, " decision under phase c (warp0): logic %.0f, z out %.0f; claims+publish in round 2 %.0f; finished/pass %.2f",
               (double)prof[11] / (double)prof[0], (double)prof[12] / (double)prof[0], (double)prof[10] / (double)prof[0],
               (double)prof[14] / (double)prof[0]);
-      fprintf(stderr, "\n");
-      memset(prof, 0, 16 * sizeof(long long));
+      fprintf(stderr, "; passes per group: max %lld mean %.1f over %lld groups; prologue %lld cycles\n", prof[16],
+              prof[18] ? (double)prof[17] / (double)prof[18] : 0.0, prof[18], prof[19]);
+      fprintf(stderr, "[tc prof] main-loop cycles, max over CTAs, by group: %lld %lld %lld\n", prof[20], prof[21], prof[22]);
+      memset(prof, 0, 24 * sizeof(long long));
     }
     if (e != cudaSuccess) {
       set_error("filter (tensor core, KP=%d C=%d): launch failed: %s", KP, C, cudaGetErrorString(e));
