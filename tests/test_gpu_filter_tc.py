@@ -1,6 +1,6 @@
 """GPU: the tensor-core ADM filter (csrc/filter_tc.cu) against the FP64 oracle and the SIMT kernel.
 
-Covers the three variants (two slot groups for k <= 112; one group with two phase-c M tiles
+Covers the variants (three slot groups for k <= 112, two with L1F_TC_NG=2; one group with two phase-c M tiles
 for 112 < k <= 160; one group with the phase-a dictionary in TMEM and the residual-form z step
 for 160 < k <= 224), cluster sizes 1..16, slot refills (many more units than slots) with dead units
 in between, the e output, max_iter status codes, and bitwise independence of unit order.
@@ -111,6 +111,23 @@ def test_tc_results_independent_of_unit_order(k):
             assert torch.equal(f[torch.from_numpy(perm)], p)
     sub = _run(x[:, 100:140], a)
     assert torch.equal(sub[0], full[0][100:140])
+
+
+@pytest.mark.parametrize("s,k,n,want_e", [(1000, 100, 1500, False), (300, 40, 800, True), (2000, 112, 400, False)])
+def test_tc_three_and_two_slot_groups_bitwise_equal(s, k, n, want_e):
+    # k <= 112 runs three slot groups per CTA (x in TMEM, 8-slot blocks); L1F_TC_NG=2 forces the
+    # two-group layout.  A unit's arithmetic does not depend on its group or slot.
+    rng = np.random.default_rng(s + k)
+    a, x = _units(rng, s, k, n)
+    three = _run(x, a, want_e=want_e)
+    os.environ["L1F_TC_NG"] = "2"
+    try:
+        two = _run(x, a, want_e=want_e)
+    finally:
+        del os.environ["L1F_TC_NG"]
+    for f, p in zip(three, two):
+        if f is not None:
+            assert torch.equal(f, p)
 
 
 def test_tc_filter_few_units_many_slots():
