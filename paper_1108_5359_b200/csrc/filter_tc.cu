@@ -80,6 +80,7 @@ struct Group {
   long long head, tail, pf_from, pf_to;
   alignas(8) unsigned long long bar_p, bar_q, bar_r, bar_a, bar_c;
   uint32_t fmask;
+  uint32_t zfin;      // slots finished at this pass (decision part 1): their z goes to 0 in round 2
   uint32_t zmask[2];  // TA: by pass parity, slots whose z_it is 0 (fresh or empty)
 };
 
@@ -543,7 +544,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
         const float tn = pr.y;
         const float x = xr[j];
-        const float azv = pr.z != 0.f ? 0.f : az[j];
+        const float azv = (TA && pr.z != 0.f) ? 0.f : az[j];  // non-TA: z = 0 for fresh/empty slots
         const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
         rmax[j] = fabsf(r);
         const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -614,7 +615,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
           const float tn = pr.y;
           const float x = xb[i];
-          const float azv = pr.z != 0.f ? 0.f : az[i];
+          const float azv = (TA && pr.z != 0.f) ? 0.f : az[i];  // non-TA: z = 0 for fresh/empty slots
           const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
           rmax[i] = fabsf(r);
           const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -742,6 +743,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         }
       }
       fmask = __ballot_sync(0xffffffffu, fin);
+      if (lane == 0) G.zfin = fmask;  // read by round 2 after the group barrier
       const long long tdec1 = pdec ? clock64() : 0;
       const float* zsp = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
       for (unsigned mm = fmask; mm; mm &= mm - 1) {  // my slice of z_it of every finished unit
@@ -931,6 +933,13 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           }
         }
         stamp(7);
+        if constexpr (!TA) {  // slots finished at this pass restart (refill) or idle with z = 0
+          const uint32_t zf = G.zfin >> (8 * sg);
+          if (zf & 0xFFu) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v8[i] = ((zf >> i) & 1u) ? 0.f : v8[i];
+          }
+        }
         uint4 w0, w1, w2;
         split8(v8, w0, w1, w2);
         const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
