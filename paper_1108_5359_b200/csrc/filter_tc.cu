@@ -251,7 +251,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   constexpr int GT = NT / NG;              // threads per group
   constexpr int WPG = GT / 32;             // warps per group (4 per TMEM lane quarter at NG = 1)
   constexpr int SPT = TS * 4 / WPG;        // slots per thread in phase b (32 at NG = 3, 16 at NG = 2, 8 at NG = 1)
-  constexpr int BS = SPT > 16 ? 8 : SPT;   // slots per TMEM-load block (bounds the registers)
+  constexpr int BS = SPT > 16 ? 8 : SPT;   // slots per TMEM-load block in phase b (bounds the registers)
+  constexpr int BR = SPT > 16 ? 16 : SPT;  // slots per TMEM-load block in round 1 (less state live)
   constexpr int MTC = (KP + 127) / 128;    // phase-c M tiles (over the dictionary columns)
   constexpr uint32_t ACOLS = TA ? (3u * KP / 2 + 31u) / 32u * 32u : 0u;  // TMEM columns of the TA dictionary
   // phase c reuses the phase-a columns (az is read out before phase c is issued): 96 per M tile
@@ -814,36 +815,36 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const int zr = crank * rs + row;
         float* drow = zin + (size_t)zr * TSP;
   #pragma unroll
-        for (int bk = 0; bk < SPT / BS; ++bk) {
-          const int sb = slot0 + BS * bk;
-          float zp[BS];
+        for (int bk = 0; bk < SPT / BR; ++bk) {
+          const int sb = slot0 + BR * bk;
+          float zp[BR];
           if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
-            float b0[BS], b1[BS];
+            float b0[BR], b1[BR];
             const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)sb;
-            if constexpr (BS == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
+            if constexpr (BR == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
             else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); }
             umma::ld_wait();
   #pragma unroll
-            for (int j = 0; j < BS; ++j) zp[j] = b1[j] + b0[j];
+            for (int j = 0; j < BR; ++j) zp[j] = b1[j] + b0[j];
           } else {
-            float b0[BS], b1[BS], b2[BS];
+            float b0[BR], b1[BR], b2[BR];
             const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)sb;
-            if constexpr (BS == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
+            if constexpr (BR == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
             else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
             umma::ld_wait();
   #pragma unroll
-            for (int j = 0; j < BS; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
+            for (int j = 0; j < BR; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
           }
           if (t < KP) {
             if (owner == crank) {
   #pragma unroll
-              for (int i = 0; i < BS / 4; ++i)
+              for (int i = 0; i < BR / 4; ++i)
                 *reinterpret_cast<float4*>(drow + 4 * ((sb / 4 + i) ^ (zr & 7))) =
                     make_float4(zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3]);
             } else {
               const uint32_t prow = peer_addr(umma::saddr(drow), owner), pbar = peer_addr(bar_p, owner);
   #pragma unroll
-              for (int i = 0; i < BS / 4; ++i)
+              for (int i = 0; i < BR / 4; ++i)
                 st_async16v(prow + 16 * ((sb / 4 + i) ^ (zr & 7)), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2], zp[4 * i + 3],
                             pbar);
             }
