@@ -57,7 +57,7 @@ struct Smem {
   unsigned long long full[STAGES], empty[STAGES];
   unsigned long long tfull[2], tempty[2];
   unsigned long long mfull[NMB];
-  float colscale[2][BN];  // 2^-eb of the tile's columns, by tile parity
+  alignas(16) float colscale[2][BN];  // 2^-eb of the tile's columns, by tile parity
   uint32_t tmem_base;
   double red[2][8];
 };
