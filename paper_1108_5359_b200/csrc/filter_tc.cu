@@ -3,9 +3,9 @@
 //
 // Reference: _solve_block, pkg/src/l1pcp/l1reg.py:59-137 (per-unit ADM for min ||x - A z||_1).
 // A cluster of C = ceil(s / 128) CTAs keeps the s x k dictionary resident (CTA c: rows
-// [128 c, 128 c + 128)).  Each CTA runs NG independent slot groups of 32 units (NG = 2 for
-// k <= 112: warps 0-7 and 8-15; NG = 1 for larger k); a group's pass is one ADM iteration of its
-// 32 units:
+// [128 c, 128 c + 128)).  Each CTA runs NG independent slot groups of 32 units (NG = 3 for
+// k <= 112: 3 x 4 warps; NG = 2 with L1F_TC_NG=2 or when three do not fit: 2 x 8 warps; NG = 1
+// for larger k: 16 warps); a group's pass is one ADM iteration of its 32 units:
 //   phase a   az[row][slot] = sum_t A[row][t] z[t][slot]      tcgen05.mma M=128 (rows) N=32 K=k
 //   phase b   the elementwise ADM update of filter_resident.cu (cancellation-free residual)
 //   phase c   zp[t][slot]   = sum_row A[row][t] v[row][slot]   tcgen05.mma M=128 (t)    N=32 K=128
@@ -13,22 +13,24 @@
 //             (DSMEM st.async) with the per-slot max|r|; the per-unit decision follows; round 2:
 //             owners sum their slice, split it into the bf16 pieces of the phase-a operand and
 //             push those to every CTA.
-// The two groups share the dictionary and the tensor core; one group's MMAs overlap the other
-// group's elementwise work and DSMEM latency.
+// The groups share the dictionary and the tensor core; one group's MMAs overlap the others'
+// elementwise work and DSMEM latency.  To fit a third group the z and v operands share one buffer,
+// phase c accumulates into the phase-a TMEM columns and the slots' x live in TMEM.
 //
 // FP32 accuracy from BF16 tensor cores: every operand is split into three bf16 pieces
 // x = x0 + x1 + x2 (each the bf16 rounding of the remainder; 24 significant bits) and the
 // products with i + j <= 2 are accumulated in FP32 in TMEM (the dropped terms are ~2^-26
 // relative).  The z / v operand holds its pieces side by side along N, so one MMA per dictionary
 // piece and K step computes a0 [z0 z1 z2], a1 [z0 z1], a2 [z0] into three column blocks that hold
-// the products of order 0, 1 and 2 (summed after tcgen05.ld).  bf16 because tcgen05 reads bf16 operands in MN-major layout (TF32 only
-// K-major, tools/umma_debug.cu): the dictionary's no-swizzle core matrices (8 rows x 8 columns,
+// the products of order 0, 1 and 2 (summed after tcgen05.ld).  bf16 because tcgen05 reads bf16
+// operands in MN-major layout (TF32 only K-major, tools/umma_debug.cu): the dictionary's no-swizzle core matrices (8 rows x 8 columns,
 // 16-byte rows) are K-major for phase a (M = rows) and MN-major for phase c (M = columns), so ONE
 // resident copy of A (3 pieces, 6 B per element) serves both contractions.
 //
 // Roles in a group: warp 1 lane 0 issues the MMAs, warp 0 takes the per-slot decisions, all warps
-// do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows; 16 slots per thread at NG = 2, 8 at
-// NG = 1).  Profiling: L1F_TC_PROF=1 prints clock64 phase times of one thread (CTA 0, group 0).
+// do phase b (warp w: TMEM lanes 32 (w % 4) .. +31 = rows; 32 slots per thread at NG = 3 in
+// blocks of 8, 16 at NG = 2, 8 at NG = 1).  Profiling: L1F_TC_PROF=1 prints clock64 phase times
+// of one thread (CTA 0, group 0), the pass-count spread over groups and per-group loop cycles.
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -348,7 +350,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 
   // ================================================================ one slot group
   const int g = warp / WPG, gw = warp % WPG, gtid = tid % GT;
-  const int gbar = 1 + g, sbar = 3 + g;  // named barriers: whole group / warps 1-7 of the group
+  const int gbar = 1 + g;  // named barrier of the group (0 is __syncthreads)
   Group& G = groups[g];
   unsigned char* gb = smem_raw + Lo.group0 + g * Lo.gstride;
   __nv_bfloat16* zop = reinterpret_cast<__nv_bfloat16*>(gb + Lo.zop);  // [3][KP*TS] phase-a operand
