@@ -5,7 +5,8 @@ Configs 1 and 2 are compared in full; configs 3, 4 and 5 through the sampled ora
 8(c'): the oracle solves the seed (FP64, the reference's index draw) and filters only the sampled
 non-seed rows/columns, which yields L and S exactly on the sampled sub-block.  Gate: relative
 Frobenius difference <= 1e-4 for L and S (north_star FP32 tolerance).  Config 5 (120 GB of
-device memory for M, L, S and a 2000^2 numpy seed solve, ~40 s) can be skipped with
+device memory for M, L, S, a 2000^2 numpy seed solve and 1000 + 1000 sampled FP64 filter units,
+~40 s) can be skipped with
 L1F_SKIP_CFG5=1.
 """
 
@@ -95,4 +96,4 @@ def test_config4_sampled_parity():
 
 @pytest.mark.skipif(os.environ.get("L1F_SKIP_CFG5") == "1", reason="L1F_SKIP_CFG5=1")
 def test_config5_sampled_parity():
-    _sampled(5, 100, 100)
+    _sampled(5, 1000, 1000)  # BASELINE.json: "Oracle check on 1000 sampled columns and rows"
