@@ -482,8 +482,21 @@ def recovery_error(cfgd, l_out):
     return {"value": out, "rows_checked": rows}
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: library output written straight to file descriptor 1
+    (e.g. NCCL's version banner at communicator setup) is sent to stderr instead."""
+    try:
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(saved, "w", buffering=1)
+    except OSError:
+        pass
+
+
 def main():
     args = parse()
+    _json_stdout()
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
