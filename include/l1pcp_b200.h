@@ -84,6 +84,21 @@ int l1f_filter_f64(const double* X, int64_t ldx, int32_t s, int64_t n_units,
                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Column and row filtering in one call — filter_columns + filter_rows (l1filter.py:116-134)
+ * as the pipeline runs them (l1filter.py:244-245), fp32, no e output.  Unit set 1 (X1, A1)
+ * and unit set 2 (X2, A2) share s and k.  With the tensor-core kernel the two sets can run in
+ * one grid, the clusters split in proportion to their sizes, so the drains at the end of the
+ * two sets overlap; mode 0 lets the library choose by its pass-count model, 1 forces one
+ * launch, 2 two launches.  Per-unit results are bitwise those of two l1f_filter_f32 calls.
+ * ---------------------------------------------------------------------------------- */
+int l1f_filter_pair_f32(const float* X1, int64_t ldx1, int64_t n1, const float* A1, int64_t lda1,
+                        float* Z1, int64_t ldz1, int32_t* iters1, float* res1, uint8_t* status1,
+                        const float* X2, int64_t ldx2, int64_t n2, const float* A2, int64_t lda2,
+                        float* Z2, int64_t ldz2, int32_t* iters2, float* res2, uint8_t* status2,
+                        int32_t s, int32_t k, float tol, float rho, float beta0, float beta_max,
+                        int32_t max_iter, int32_t mode, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Index gather — replaces `m[np.ix_(rows, cols)]` (l1filter.py:87 sample_submatrix,
  * :242-243 panel extraction).  out[r][c] = M[rows[r]][cols[c]] (transpose=0) or
  * out[c][r] (transpose=1, the unit-major column panel).  rows/cols may be NULL (= arange).

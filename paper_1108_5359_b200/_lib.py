@@ -59,6 +59,9 @@ SIGNATURES = {
                               _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "l1f_filter_f64": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f64, _f64, _f64, _f64, _i32,
                               _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "l1f_filter_pair_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
+                                   _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
+                                   _i32, _i32, _f32, _f32, _f32, _f32, _i32, _i32, _vp]),
     "l1f_gather": (_int, [_int, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp, _i64, _i32, _vp]),
     "l1f_build_factors": (_int, [_int, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
                                  _vp, _i64, _vp, _i64, _vp, _vp, _vp]),

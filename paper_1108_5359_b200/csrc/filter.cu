@@ -21,9 +21,14 @@
 //    bitwise identical for any unit partition (the reference's chunk-invariance contract,
 //    l1reg.py:183-186, test_l1reg.py:63-72).
 #include "common.cuh"
+#include "filter_pair.cuh"
 
 #include <algorithm>
 #include <cstdlib>
+
+int l1f_tc_pair_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
+                         double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
+                         int32_t* iters, float* res, uint8_t* status, const l1f::tcf::Second& two, cudaStream_t st);
 
 namespace l1f {
 namespace filt {
@@ -524,4 +529,30 @@ extern "C" int l1f_filter_f64(const double* X, int64_t ldx, int32_t s, int64_t n
                               double* res, uint8_t* status, void* workspace, size_t workspace_bytes, void* stream) {
   return filt::filter_entry<double>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E,
                                     lde, iters, res, status, workspace, workspace_bytes, stream);
+}
+
+extern "C" int l1f_filter_pair_f32(const float* X1, int64_t ldx1, int64_t n1, const float* A1, int64_t lda1, float* Z1,
+                                   int64_t ldz1, int32_t* iters1, float* res1, uint8_t* status1, const float* X2,
+                                   int64_t ldx2, int64_t n2, const float* A2, int64_t lda2, float* Z2, int64_t ldz2,
+                                   int32_t* iters2, float* res2, uint8_t* status2, int32_t s, int32_t k, float tol,
+                                   float rho, float beta0, float beta_max, int32_t max_iter, int32_t mode,
+                                   void* stream) {
+  L1F_REQUIRE(s >= 1 && k >= 1 && n1 >= 0 && n2 >= 0, L1F_ERR_ARG, "filter_pair: need s >= 1, k >= 1, n >= 0");
+  L1F_REQUIRE((n1 == 0 || (ldx1 >= s && ldz1 >= k && lda1 >= k)) && (n2 == 0 || (ldx2 >= s && ldz2 >= k && lda2 >= k)),
+              L1F_ERR_ARG, "filter_pair: leading dimension too small");
+  L1F_REQUIRE(n1 < (int64_t)INT32_MAX && n2 < (int64_t)INT32_MAX, L1F_ERR_UNSUPPORTED, "filter_pair: too many units");
+  L1F_REQUIRE(rho > 1.f && tol > 0.f, L1F_ERR_ARG, "filter_pair: need rho > 1 and tol > 0");
+  L1F_REQUIRE(mode >= 0 && mode <= 2, L1F_ERR_ARG, "filter_pair: mode must be 0, 1 or 2");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n1 > 0 && n2 > 0 && !filt::force_streaming()) {
+    const tcf::Second two{X2, ldx2, n2, A2, lda2, Z2, ldz2, iters2, res2, status2, mode};
+    const int rc = l1f_tc_pair_dispatch(X1, ldx1, s, n1, A1, lda1, k, tol, rho, beta0, beta_max, max_iter, Z1, ldz1,
+                                        iters1, res1, status1, two, st);
+    if (rc != L1F_ERR_UNSUPPORTED) return rc;
+  }
+  int rc = l1f_filter_f32(X1, ldx1, s, n1, A1, lda1, k, tol, rho, beta0, beta_max, max_iter, Z1, ldz1, nullptr, s,
+                          iters1, res1, status1, nullptr, 0, stream);
+  if (rc != L1F_OK) return rc;
+  return l1f_filter_f32(X2, ldx2, s, n2, A2, lda2, k, tol, rho, beta0, beta_max, max_iter, Z2, ldz2, nullptr, s, iters2,
+                        res2, status2, nullptr, 0, stream);
 }

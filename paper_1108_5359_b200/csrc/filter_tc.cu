@@ -32,6 +32,7 @@
 // blocks of 8, 16 at NG = 2, 8 at NG = 1).  Profiling: L1F_TC_PROF=1 prints clock64 phase times
 // of one thread (CTA 0, group 0), the pass-count spread over groups and per-group loop cycles.
 #include "common.cuh"
+#include "filter_pair.cuh"
 #include "umma.cuh"
 
 #include <cuda_bf16.h>
@@ -64,6 +65,21 @@ struct Params {
   int64_t n_units, ldx, ldz, lde;
   int max_iter;
   double tol, rho, beta0, beta_max;
+};
+
+// second unit set of a paired launch (column and row filters in one grid): clusters
+// [nc0, nclusters) take it; nc0 = 0 means a single unit set
+struct Pair {
+  const float* X;
+  const float* A;
+  int64_t lda;
+  const float* scale;
+  int64_t n_units, ldx, ldz;
+  float* Z;
+  int32_t* iters;
+  float* res;
+  uint8_t* status;
+  int nc0;
 };
 
 // dynamic shared memory: dictionary pieces, then one region per group (byte offsets)
@@ -246,7 +262,7 @@ template <int KP, int NG, int NA, bool TA>
 __global__ void __launch_bounds__(threads_of(NG), 1)
 adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t lda, const float* __restrict__ scale,
               Params P, Layout Lo, float* __restrict__ Z, float* __restrict__ E, int32_t* __restrict__ iters,
-              float* __restrict__ res_out, uint8_t* __restrict__ status, long long* __restrict__ prof) {
+              float* __restrict__ res_out, uint8_t* __restrict__ status, long long* __restrict__ prof, Pair Q) {
   constexpr int KG = KP / 8;
   constexpr int NT = threads_of(NG);
   constexpr int RNG = ring_of(NG);
@@ -277,7 +293,18 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   const long long t_entry = clock64();
   const int C = P.cluster;
   const int crank = C > 1 ? (int)cluster.block_rank() : 0;
-  const int cid = blockIdx.x / C, nclusters = gridDim.x / C;
+  int cid = blockIdx.x / C, nclusters = gridDim.x / C;
+  if (Q.nc0 > 0) {  // paired launch: clusters [0, nc0) take the first unit set, the rest the second
+    if (cid >= Q.nc0) {
+      cid -= Q.nc0;
+      nclusters -= Q.nc0;
+      X = Q.X; A = Q.A; lda = Q.lda; scale = Q.scale;
+      P.n_units = Q.n_units; P.ldx = Q.ldx; P.ldz = Q.ldz;
+      Z = Q.Z; iters = Q.iters; res_out = Q.res; status = Q.status;
+    } else {
+      nclusters = Q.nc0;
+    }
+  }
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row_base = crank * SL;
   const float tol = (float)P.tol, rho = (float)P.rho;
@@ -1089,7 +1116,9 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
       cudaMallocManaged(&prof, 24 * sizeof(long long));
       memset(prof, 0, 24 * sizeof(long long));
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof);
+    Pair Q = {};
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof,
+                                       Q);
     if (prof) {
       cudaStreamSynchronize(st);
       const char* names[10] = {"passes", "a:mma", "phase b", "c:mma", "ld+push1", "wait1", "sumloop", "split", "store+push2", "wait2+bar_or"};
@@ -1112,6 +1141,96 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     set_error("filter: prologue launch failed");
   }
   if (owned) cudaFreeAsync(owned, st);
+  return rc;
+}
+
+// Column and row filters in one grid: clusters split between the two unit sets in proportion to
+// their sizes, so the drains at the end of the two sets overlap.  A group's pass count is about
+// units / slots * (mean iterations) + (drain of the last units), so one launch wins when the
+// unit sets are small next to the slots (multi-GPU shards, cfg2) and loses to the cluster-split
+// imbalance when they are large.  Per-unit results are identical either way.
+template <int KP, int NG, int NA, bool TA = false>
+int launch_pair(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k, double tol,
+                double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz, int32_t* iters, float* res,
+                uint8_t* status, const Second& two, cudaStream_t st) {
+  const int C = (int)ceil_div(s, SL);
+  const int rs = (int)ceil_div(KP, C);
+  const Layout Lo = make_layout<KP, NG, NA, TA>(C, rs);
+  auto kern = adm_tc_kernel<KP, NG, NA, TA>;
+  static bool configured = false;
+  if (!configured) {
+    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit(NG)));
+    L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads_of(NG), 1, 1);
+  cfg.dynamicSmemBytes = Lo.total;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(C, 1, 1);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    max_clusters = std::max(1, num_sms() / C);
+  const int64_t n1 = n_units, n2 = two.n_units;
+  const double slots = (double)TS * NG;
+  const int64_t want1 = ceil_div(n1, (int64_t)TS * NG), want2 = ceil_div(n2, (int64_t)TS * NG);
+  const int total = (int)std::min<int64_t>(max_clusters, want1 + want2);
+  int nc0 = (int)std::llround((double)total * (double)n1 / (double)std::max<int64_t>(1, n1 + n2));
+  nc0 = std::max(1, std::min(total - 1, nc0));
+  auto passes = [&](double n, double c) { return n / (c * slots) * 25.0 + 36.0; };
+  const double seq = passes((double)n1, (double)std::min<int64_t>(max_clusters, std::max<int64_t>(1, want1))) +
+                     passes((double)n2, (double)std::min<int64_t>(max_clusters, std::max<int64_t>(1, want2)));
+  const double one = std::max(passes((double)n1, nc0), passes((double)n2, total - nc0));
+  const bool paired = n1 > 0 && n2 > 0 && max_iter > 0 && total >= 2 && two.mode != 2 && (two.mode == 1 || one < seq);
+  if (!paired) {
+    int rc = launch<KP, NG, NA, TA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, nullptr,
+                                    s, iters, res, status, nullptr, 0, st, false, nullptr);
+    if (rc != L1F_OK) return rc;
+    return launch<KP, NG, NA, TA>(two.X, two.ldx, s, two.n_units, two.A, two.lda, k, tol, rho, beta0, beta_max, max_iter,
+                                  two.Z, two.ldz, nullptr, s, two.iters, two.res, two.status, nullptr, 0, st, false,
+                                  nullptr);
+  }
+  const size_t b1 = (sizeof(float) * (size_t)n1 + 255) & ~(size_t)255;
+  float* scale = nullptr;
+  L1F_CUDA_TRY(cudaMallocAsync(&scale, b1 + sizeof(float) * (size_t)n2, st));
+  float* scale2 = reinterpret_cast<float*>(reinterpret_cast<char*>(scale) + b1);
+  Params P;
+  P.s = s; P.k = k; P.cluster = C; P.rs = rs;
+  P.n_units = n1; P.ldx = ldx; P.ldz = ldz; P.lde = s; P.max_iter = max_iter;
+  P.tol = tol; P.rho = rho; P.beta0 = beta0; P.beta_max = beta_max;
+  Params P2 = P;
+  P2.n_units = n2; P2.ldx = two.ldx; P2.ldz = two.ldz;
+  int rc = L1F_OK;
+  unit_scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n1, 8), 65535), 256, 0, st>>>(X, P, scale, Z, nullptr, iters,
+                                                                                         res, status);
+  unit_scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n2, 8), 65535), 256, 0, st>>>(two.X, P2, scale2, two.Z, nullptr,
+                                                                                         two.iters, two.res, two.status);
+  if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+  if (rc == L1F_OK) {
+    Pair Q;
+    Q.X = two.X; Q.A = two.A; Q.lda = two.lda; Q.scale = scale2;
+    Q.n_units = n2; Q.ldx = two.ldx; Q.ldz = two.ldz;
+    Q.Z = two.Z; Q.iters = two.iters; Q.res = two.res; Q.status = two.status;
+    Q.nc0 = nc0;
+    cfg.gridDim = dim3((unsigned)(total * C), 1, 1);
+    long long* prof = nullptr;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, (float*)nullptr, iters, res,
+                                       status, prof, Q);
+    if (e != cudaSuccess) {
+      set_error("filter pair (tensor core, KP=%d C=%d): launch failed: %s", KP, C, cudaGetErrorString(e));
+      rc = L1F_ERR_CUDA;
+    }
+  } else {
+    set_error("filter pair: prologue launch failed");
+  }
+  cudaFreeAsync(scale, st);
   return rc;
 }
 
@@ -1176,5 +1295,54 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
 #undef L1F_TA
   return L1F_ERR_UNSUPPORTED;
 #undef L1F_TC
+  return L1F_ERR_UNSUPPORTED;
+}
+
+// paired dispatch (float; same variant selection as l1f_tc_dispatch, no E output):
+// L1F_ERR_UNSUPPORTED when the tensor-core kernel does not apply to the shape
+int l1f_tc_pair_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
+                         double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
+                         int32_t* iters, float* res, uint8_t* status, const l1f::tcf::Second& two, cudaStream_t st) {
+  const char* env = getenv("L1F_FILTER_TC");
+  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  using namespace l1f::tcf;
+  if (k <= 16 || k > 224 || s > 16 * SL) return L1F_ERR_UNSUPPORTED;
+#define L1F_TCP(KP, NG, NA, TA)                                                                                  \
+  if (fits<KP, NG, NA, TA>(s))                                                                                    \
+    return launch_pair<KP, NG, NA, TA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, \
+                                       iters, res, status, two, st)
+  if (k <= 112) {
+    const char* ng = getenv("L1F_TC_NG");
+    if (!(ng && ng[0] == '2')) {
+      switch ((int)l1f::ceil_div(k, 16) * 16) {
+        case 32: L1F_TCP(32, 3, 3, false); break;
+        case 48: L1F_TCP(48, 3, 3, false); break;
+        case 64: L1F_TCP(64, 3, 3, false); break;
+        case 80: L1F_TCP(80, 3, 3, false); break;
+        case 96: L1F_TCP(96, 3, 3, false); break;
+        case 112: L1F_TCP(112, 3, 3, false); break;
+      }
+    }
+    switch ((int)l1f::ceil_div(k, 16) * 16) {
+      case 32: L1F_TCP(32, 2, 3, false); break;
+      case 48: L1F_TCP(48, 2, 3, false); break;
+      case 64: L1F_TCP(64, 2, 3, false); break;
+      case 80: L1F_TCP(80, 2, 3, false); break;
+      case 96: L1F_TCP(96, 2, 3, false); break;
+      case 112: L1F_TCP(112, 2, 3, false); break;
+    }
+    return L1F_ERR_UNSUPPORTED;
+  }
+  switch ((int)l1f::ceil_div(k, 32) * 32) {
+    case 128: L1F_TCP(128, 1, 3, false); break;
+    case 160: L1F_TCP(160, 1, 3, false); break;
+  }
+  switch ((int)l1f::ceil_div(k, 16) * 16) {
+    case 176: L1F_TCP(176, 1, 2, true); break;
+    case 192: L1F_TCP(192, 1, 2, true); break;
+    case 208: L1F_TCP(208, 1, 2, true); break;
+    case 224: L1F_TCP(224, 1, 2, true); break;
+  }
+#undef L1F_TCP
   return L1F_ERR_UNSUPPORTED;
 }

@@ -74,11 +74,15 @@ def _all_gather_rows(local, counts, group=None):
     world = len(counts)
     width = local.shape[1]
     hmax = max(max(counts), 1)
+    if world == 1:
+        return local
     pad = local.new_zeros((hmax, width))
     pad[: local.shape[0]] = local
-    bufs = [local.new_empty((hmax, width)) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
-    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+    out = local.new_empty((world * hmax, width))
+    dist.all_gather_into_tensor(out, pad, group=group)
+    if all(c == hmax for c in counts):
+        return out
+    return torch.cat([out[g * hmax:g * hmax + c] for g, c in enumerate(counts)], dim=0)
 
 
 def gather_seed_rows(m_local, plan, group=None):
@@ -235,7 +239,8 @@ class CudaShardedStep:
         nbytes = max(_lib.load().l1f_filter_workspace_bytes(code, len(plan.row_idx), self.k, max(1, len(plan.my_cols))),
                      _lib.load().l1f_filter_workspace_bytes(code, len(plan.col_idx), self.k, max(1, len(plan.my_rows))))
         self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
-        self.launches_per_step = 11  # 2 gathers, 2 x (scale prologue + filter), factors, 2 pads, reconstruct, sum
+        self._n_units_t = None
+        self.launches_per_step = 11  # 2 gathers, 2 scale prologues + 1-2 filter grids, factors, 2 splits, recon, sum
 
     def step(self, m_local, events=None):
         from .l1reg import filter_units
@@ -252,8 +257,13 @@ class CudaShardedStep:
                  dv.stream())
         if events is not None:
             events[0].record()
-        zc, _, itc, _, stc = filter_units(self.xc, self.u, self.adm, want_e=False, workspace=self.ws)
-        zr, _, itr, _, st_r = filter_units(self.xr, self.v, self.adm, want_e=False, workspace=self.ws)
+        if self.fdt == torch.float32 and self.xc.shape[1] == self.xr.shape[1] and os.environ.get("L1F_FILTER_PAIR") != "0":
+            # one call for the shard's column and row units (small shards: overlapped drains)
+            from .l1reg import filter_units_pair
+            (zc, itc, _, stc), (zr, itr, _, st_r) = filter_units_pair(self.xc, self.u, self.xr, self.v, self.adm)
+        else:
+            zc, _, itc, _, stc = filter_units(self.xc, self.u, self.adm, want_e=False, workspace=self.ws)
+            zr, _, itr, _, st_r = filter_units(self.xr, self.v, self.adm, want_e=False, workspace=self.ws)
         if events is not None:
             events[1].record()
         if self.fdt != self.dt:
@@ -269,9 +279,9 @@ class CudaShardedStep:
         it = torch.stack([itc.max() if itc.numel() else torch.zeros((), dtype=itc.dtype, device=dev),
                           itr.max() if itr.numel() else torch.zeros((), dtype=itr.dtype, device=dev)]).max()
         failed = ((stc == 1) | (stc == 2)).sum() + ((st_r == 1) | (st_r == 2)).sum()
-        stats = torch.stack([it.double(), failed.double(),
-                             torch.tensor(float(itc.numel() + itr.numel()), dtype=torch.float64, device=dev),
-                             itc.double().sum() + itr.double().sum()])
+        if self._n_units_t is None:  # a device constant: no host->device copy inside the step
+            self._n_units_t = torch.full((), float(itc.numel() + itr.numel()), dtype=torch.float64, device=dev)
+        stats = torch.stack([it.double(), failed.double(), self._n_units_t, itc.double().sum() + itr.double().sum()])
         return self.l, self.s, stats, (itc, itr)
 
 

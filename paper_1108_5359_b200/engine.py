@@ -226,8 +226,14 @@ def filter_stage(plan, mt, events=None):
     if events is not None:
         events[1].record(stream)
     ws = plan.workspace
-    zc, ec, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=plan.want_e, workspace=ws)
-    zr, er, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=plan.want_e, workspace=ws)
+    if not plan.want_e and fdt == torch.float32 and xc.shape[1] == xr.shape[1] and os.environ.get("L1F_FILTER_PAIR") != "0":
+        # one call for both filters: the library may run them in one grid (overlapped drains)
+        from .l1reg import filter_units_pair
+        (zc, itc, rc, stc), (zr, itr, rr, st_r) = filter_units_pair(xc, plan.u, xr, plan.v, plan.adm)
+        ec = er = None
+    else:
+        zc, ec, itc, rc, stc = filter_units(xc, plan.u, plan.adm, want_e=plan.want_e, workspace=ws)
+        zr, er, itr, rr, st_r = filter_units(xr, plan.v, plan.adm, want_e=plan.want_e, workspace=ws)
     if events is not None:
         events[2].record(stream)
     if fdt != mt.dtype:

@@ -80,6 +80,30 @@ def filter_units(x_um, a, cfg, want_e=True, workspace=None):
     return z, e, iters, res, status
 
 
+def filter_units_pair(x1, a1, x2, a2, cfg, mode=0):
+    """Two unit-major fp32 panels of the same width against their dictionaries in one call
+    (l1f_filter_pair_f32): the column and row filters of the pipeline.  Returns
+    ((z1, iters1, res1, status1), (z2, iters2, res2, status2)); no e output."""
+    torch = dv.torch
+    outs = []
+    for x, a in ((x1, a1), (x2, a2)):
+        n_units = x.shape[0]
+        outs.append((dv.empty((n_units, a.shape[1]), like=x), torch.empty(n_units, dtype=torch.int32, device="cuda"),
+                     dv.empty((n_units,), like=x), torch.empty(n_units, dtype=torch.uint8, device="cuda")))
+    s, k = x1.shape[1], a1.shape[1]
+    if x2.shape[1] != s or a2.shape[1] != k:
+        raise ValueError("filter_units_pair: the two panels need the same s and k")
+    beta0 = float(cfg.beta0) if cfg.beta0 is not None else 0.0
+    beta_max = float(cfg.beta_max) if cfg.beta_max is not None else 0.0
+    (z1, i1, r1, s1), (z2, i2, r2, s2) = outs
+    _lib.call("l1f_filter_pair_f32", dv.ptr(x1), max(x1.stride(0), s), x1.shape[0], dv.ptr(a1), a1.stride(0),
+              dv.ptr(z1), max(z1.stride(0), k), dv.ptr(i1), dv.ptr(r1), dv.ptr(s1), dv.ptr(x2), max(x2.stride(0), s),
+              x2.shape[0], dv.ptr(a2), a2.stride(0), dv.ptr(z2), max(z2.stride(0), k), dv.ptr(i2), dv.ptr(r2),
+              dv.ptr(s2), s, k, float(cfg.tol),
+              float(cfg.rho), beta0, beta_max, int(cfg.max_iter), int(mode), dv.stream())
+    return outs[0], outs[1]
+
+
 def workspace_bytes(dtype_code, s, k, n_units):
     return int(_lib.load().l1f_filter_workspace_bytes(dtype_code, s, k, n_units))
 
