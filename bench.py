@@ -278,14 +278,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step(evs=None):
-        f = engine.filter_stage(plan, mt, evs)
-        af, bf = engine.build_factors(plan, f["zc"], f["zr"])
-        if evs is not None:
-            evs[3].record(stream)
-        _, _, rs = engine.reconstruct(mt, af, bf, l_out, s_out)
-        if evs is not None:
-            evs[4].record(stream)
-        return f, rs
+        f = engine.solve_step(plan, mt, l_out, s_out, evs)
+        return f, f["resid_sq"]
 
     for _ in range(args.warmup):
         f, rs = step()
@@ -303,7 +297,27 @@ def run_ours(args):
     ms = start.elapsed_time(end) / args.steps
     t_filter = np.mean([e[0].elapsed_time(e[2]) for e in ev_all]) if ev_all else 0.0  # gathers excluded below
     t_filter_only = np.mean([e[1].elapsed_time(e[2]) for e in ev_all])
-    t_recon = np.mean([e[3].elapsed_time(e[4]) for e in ev_all])
+    streamed = bool(f.get("streamed"))
+    if streamed:
+        # the reconstruction runs beside the row filter; time the same kernel family alone for
+        # its HBM roofline (outside the timed steps), and report the exposed tail of the step
+        t_tail = float(np.mean([e[2].elapsed_time(e[4]) for e in ev_all]))
+        af_s, bf_s = engine.build_factors(plan, f["zc"], f["zr"])
+        ra, rb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        engine.reconstruct(mt, af_s, bf_s, l_out, s_out)
+        reps = 5
+        ra.record(stream)
+        for _ in range(reps):
+            engine.reconstruct(mt, af_s, bf_s, l_out, s_out)
+        rb.record(stream)
+        torch.cuda.synchronize()
+        t_recon = ra.elapsed_time(rb) / reps
+        del af_s, bf_s
+        f, rs = step()  # L, S of the streamed path again (the recovery check reads l_out)
+        torch.cuda.synchronize()
+    else:
+        t_recon = np.mean([e[3].elapsed_time(e[4]) for e in ev_all])
+        t_tail = t_recon
     value = m * n / (ms * 1e-3) / 1e6
 
     # algorithmic work of the dominant kernel: sum_u it_u * s * (4k + 12)
@@ -343,7 +357,22 @@ def run_ours(args):
                          f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
                          f"{m}x{n}"}
 
-    launches_per_step = 2 + 2 * 2 + 1 + 4  # gathers, (unit scale + filter) x 2, factors, split x 2 + recon + sum
+    if streamed:  # gathers, unit scale + column filter, Bf; strip index, Bf split, unit scale + row filter,
+        launches_per_step = 2 + 2 + 1 + 8  # gate, concurrent + trailing reconstruction, residual sum
+        phases = {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
+                  "column_filter": float(np.mean([e[1].elapsed_time(e[3]) for e in ev_all])),
+                  "row_filter": float(np.mean([e[3].elapsed_time(e[2]) for e in ev_all])),
+                  "filters": t_filter_only,
+                  "reconstruct_exposed": t_tail,
+                  "reconstruct_standalone": t_recon,
+                  "note": "the reconstruction of each 128-row strip runs beside the row filter on the SMs its "
+                          "clusters leave free once the strip's row units are done; the rest after it",
+                  "t1_seed_s": t1, "generate_s": t_gen}
+    else:
+        launches_per_step = 2 + 2 * 2 + 1 + 4  # gathers, (unit scale + filter) x 2, factors, split x 2 + recon + sum
+        phases = {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
+                  "filters": t_filter_only, "factors": float(np.mean([e[2].elapsed_time(e[3]) for e in ev_all])),
+                  "reconstruct": t_recon, "t1_seed_s": t1, "generate_s": t_gen}
     traffic = ncu_traffic(cfgd)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -375,9 +404,7 @@ def run_ours(args):
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                                  "traffic": traffic.get("reconstruct", {}).get("dram_bytes_per_launch"),
                                  "traffic_source": traffic.get("reconstruct", {}).get("source")},
-        "phases_ms": {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
-                      "filters": t_filter_only, "factors": float(np.mean([e[2].elapsed_time(e[3]) for e in ev_all])),
-                      "reconstruct": t_recon, "t1_seed_s": t1, "generate_s": t_gen},
+        "phases_ms": phases,
         "filter": {"units": int(f["iters_c"].numel() + f["iters_r"].numel()),
                    "mean_iters": (itc + itr) / max(1, f["iters_c"].numel() + f["iters_r"].numel()),
                    "max_iters": int(max(f["iters_c"].max().item(), f["iters_r"].max().item())),

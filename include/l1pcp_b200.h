@@ -98,6 +98,10 @@ int l1f_filter_pair_f32(const float* X1, int64_t ldx1, int64_t n1, const float* 
                         int32_t s, int32_t k, float tol, float rho, float beta0, float beta_max,
                         int32_t max_iter, int32_t mode, void* stream);
 
+/* Whether l1f_filter_pair_f32 (mode 0) would run the two unit sets in one grid: *one_grid = 1
+ * or 0 (0 also when the tensor-core kernel does not apply).  No device work. */
+int l1f_filter_pair_plan_f32(int32_t s, int32_t k, int64_t n1, int64_t n2, int32_t* one_grid);
+
 /* ------------------------------------------------------------------------------------
  * Index gather — replaces `m[np.ix_(rows, cols)]` (l1filter.py:87 sample_submatrix,
  * :242-243 panel extraction).  out[r][c] = M[rows[r]][cols[c]] (transpose=0) or
@@ -135,6 +139,32 @@ int l1f_reconstruct(int dtype, int64_t m, int64_t n, int32_t k,
                     const void* Af, int64_t ldaf, const void* Bf, int64_t ldbf,
                     const void* M, int64_t ldm, void* L, int64_t ldl, void* S, int64_t lds,
                     double* resid_sq, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Row filtering and reconstruction, overlapped — filter_rows (l1filter.py:125-134) followed
+ * by assemble + s = m - l (l1filter.py:151-167,253), for the fp32 tensor-core path.
+ * Runs the row units X (the m - s_r non-seed rows of M, in order; unit_rows[u] = their row
+ * index, i.e. comp_rows) against V exactly as l1f_filter_f32 (no e output), then
+ *   L = Af Bf^T, S = M - L, resid_sq as l1f_reconstruct,
+ * with Af built from (row_idx, U, sigma, Zr) and Bf from (col_idx, sigma, V64, Zc = the column
+ * filter's z) as l1f_build_factors does.  L and S are bitwise those of l1f_filter_f32 +
+ * l1f_build_factors + l1f_reconstruct.  Bf, its pieces and the reconstruction of each 128-row
+ * strip run on the SMs the filter's clusters leave free, a strip as soon as its row units are
+ * finished; the rest follows the filter on every SM.
+ * ev_filter_done (a cudaEvent_t, nullable) is recorded on `stream` after the filter launch.
+ * Returns L1F_ERR_UNSUPPORTED (nothing to undo; call the three functions instead) when the
+ * tensor-core filter or reconstruction does not apply (k <= 16, k > 224, alignment).
+ * ---------------------------------------------------------------------------------- */
+int l1f_rowfilter_reconstruct_f32(const float* X, int64_t ldx, int32_t s, int64_t n_units,
+                                  const float* V, int64_t ldv, int32_t k, float tol, float rho,
+                                  float beta0, float beta_max, int32_t max_iter,
+                                  float* Zr, int64_t ldz, int32_t* iters, float* res, uint8_t* status,
+                                  const int64_t* unit_rows, const int64_t* row_idx, int64_t s_r,
+                                  const double* U, const double* sigma, const int64_t* col_idx,
+                                  int64_t s_c, const double* V64, const float* Zc, int64_t ldzc,
+                                  const float* M, int64_t m, int64_t n, int64_t ldm,
+                                  float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
+                                  void* ev_filter_done, void* stream);
 
 /* General C = alpha * A B^T (+ beta*C), A m x k, B n x k, row-major; used for the small
  * dense products of the reference API (SkinnySvd.reconstruct matcore.py:36-38,

@@ -62,11 +62,16 @@ SIGNATURES = {
     "l1f_filter_pair_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
                                    _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
                                    _i32, _i32, _f32, _f32, _f32, _f32, _i32, _i32, _vp]),
+    "l1f_filter_pair_plan_f32": (_int, [_i32, _i32, _i64, _i64, _vp]),
     "l1f_gather": (_int, [_int, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp, _i64, _i32, _vp]),
     "l1f_build_factors": (_int, [_int, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _vp,
                                  _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "l1f_reconstruct": (_int, [_int, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                _vp, _i64, _vp, _vp]),
+    "l1f_rowfilter_reconstruct_f32": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _i32,
+                                             _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
+                                             _vp, _i64,
+                                             _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "l1f_gemm_nt": (_int, [_int, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _vp]),
     "l1f_generate_factors_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "l1f_generate_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _f32, _f32, _vp, _vp, _i64, _i64,

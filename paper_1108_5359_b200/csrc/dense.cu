@@ -345,6 +345,7 @@ __global__ void build_factors_kernel(int64_t m, int64_t n, int k, const int64_t*
       const int64_t p = lower_bound_i64(row_idx, s_r, i);
       T v;
       if (p < s_r && row_idx[p] == i) v = (T)U[p * k + t];
+      else if (sizeof(T) == 4) v = (T)(Zr[(i - p) * ldzr + t] * (T)(1.0 / sigma[t]));  // = recon_tc.cu split_rows
       else v = (T)((double)Zr[(i - p) * ldzr + t] / sigma[t]);
       Af[i * k + t] = v;
     } else {

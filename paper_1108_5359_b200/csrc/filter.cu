@@ -545,7 +545,7 @@ extern "C" int l1f_filter_pair_f32(const float* X1, int64_t ldx1, int64_t n1, co
   L1F_REQUIRE(mode >= 0 && mode <= 2, L1F_ERR_ARG, "filter_pair: mode must be 0, 1 or 2");
   cudaStream_t st = (cudaStream_t)stream;
   if (n1 > 0 && n2 > 0 && !filt::force_streaming()) {
-    const tcf::Second two{X2, ldx2, n2, A2, lda2, Z2, ldz2, iters2, res2, status2, mode};
+    const tcf::Second two{X2, ldx2, n2, A2, lda2, Z2, ldz2, iters2, res2, status2, mode, nullptr};
     const int rc = l1f_tc_pair_dispatch(X1, ldx1, s, n1, A1, lda1, k, tol, rho, beta0, beta_max, max_iter, Z1, ldz1,
                                         iters1, res1, status1, two, st);
     if (rc != L1F_ERR_UNSUPPORTED) return rc;
@@ -555,4 +555,16 @@ extern "C" int l1f_filter_pair_f32(const float* X1, int64_t ldx1, int64_t n1, co
   if (rc != L1F_OK) return rc;
   return l1f_filter_f32(X2, ldx2, s, n2, A2, lda2, k, tol, rho, beta0, beta_max, max_iter, Z2, ldz2, nullptr, s, iters2,
                         res2, status2, nullptr, 0, stream);
+}
+
+extern "C" int l1f_filter_pair_plan_f32(int32_t s, int32_t k, int64_t n1, int64_t n2, int32_t* one_grid) {
+  L1F_REQUIRE(s >= 1 && k >= 1 && n1 >= 0 && n2 >= 0 && one_grid, L1F_ERR_ARG, "filter_pair_plan: bad arguments");
+  *one_grid = 0;
+  if (n1 == 0 || n2 == 0 || filt::force_streaming()) return L1F_OK;
+  int plan = 0;
+  tcf::Second two{nullptr, s, n2, nullptr, k, nullptr, k, nullptr, nullptr, nullptr, 3, &plan};
+  const int rc = l1f_tc_pair_dispatch(nullptr, s, s, n1, nullptr, k, k, 1e-7, 1.5, 0.0, 0.0, 1000, nullptr, k, nullptr,
+                                      nullptr, nullptr, two, nullptr);
+  if (rc == L1F_OK) *one_grid = plan;
+  return rc == L1F_ERR_UNSUPPORTED ? L1F_OK : rc;
 }

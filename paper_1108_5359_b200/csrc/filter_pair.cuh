@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 namespace l1f {
 namespace tcf {
 
@@ -15,8 +17,20 @@ struct Second {
   int32_t* iters;
   float* res;
   uint8_t* status;
-  int mode;  // 0: by the pass model, 1: one launch, 2: two launches
+  int mode;  // 0: by the pass model, 1: one launch, 2: two launches, 3: report the model's choice only
+  int* plan_out = nullptr;  // mode 3: 1 if one grid would run, else 0
 };
+
+// host side: progress-notification targets of the next single-set launch on this thread
+// (l1f_rowfilter_reconstruct_f32), and what that launch did
+struct NotifyHost {
+  const int64_t* rows = nullptr;    // output row of every unit (strip = row >> 7)
+  unsigned* cnt = nullptr;          // per strip: + 1 per (unit, CTA of its cluster) with z written
+  unsigned* resident = nullptr;     // + 1 per started CTA
+  cudaEvent_t after_prologue = nullptr;  // recorded between the prologue and the main launch
+  int cluster = 0, ctas = 0;        // out: cluster size, CTAs of the main launch (0: none)
+};
+extern thread_local NotifyHost* g_notify;
 
 }  // namespace tcf
 }  // namespace l1f

@@ -80,7 +80,15 @@ struct Pair {
   float* res;
   uint8_t* status;
   int nc0;
+  // progress notification for a concurrent consumer (l1f_rowfilter_reconstruct_f32): the CTA count
+  // of the launch is added to *nres as the CTAs start, and every CTA adds 1 to ncnt[nrows[u] >> 7]
+  // once its slice of z_u is in global memory (null: off; single unit set only)
+  const int64_t* nrows;
+  unsigned* ncnt;
+  unsigned* nres;
 };
+
+thread_local NotifyHost* g_notify = nullptr;
 
 // dynamic shared memory: dictionary pieces, then one region per group (byte offsets)
 struct Layout {
@@ -306,6 +314,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     }
   }
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  if (Q.nres && tid == 0) atomicAdd(Q.nres, 1u);
   const int row_base = crank * SL;
   const float tol = (float)P.tol, rho = (float)P.rho;
   const int rs = P.rs;                              // z rows owned (summed) by each CTA
@@ -509,6 +518,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 
   uint32_t ph_a = 0, ph_c = 0, ph_x = 0, par = 0;
   long long npass = 0;
+  int pend = -1;  // decision lane: strip of the unit whose z slice it wrote at the last pass (notification)
   if (prof != nullptr && blockIdx.x == 0 && tid == 0) prof[19] = clock64() - t_entry;  // prologue
   const long long t_loop = clock64();
   const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 64;  // profile: one thread of CTA 0, group 0
@@ -737,6 +747,13 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
       // MMAs run: stop tests, outputs of finished units (iters, residual, status, z slice), beta schedule
       const long long tdec0 = pdec ? clock64() : 0;
       const int slot = lane;
+      if (Q.ncnt && __any_sync(0xffffffffu, pend >= 0)) {  // z slices written at the last pass
+        if (pend >= 0) {
+          __threadfence();
+          atomicAdd(&Q.ncnt[pend], 1u);
+        }
+        pend = -1;
+      }
       bool fin = false;
       float r = 0.f;
       for (int c = 0; c < C; ++c) r = fmaxf(r, rall_p[c * TS + slot]);
@@ -782,6 +799,9 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         for (int row = lane; row < vmine; row += 32)
           if (r0 + row < P.k) Z[u * P.ldz + r0 + row] = zsp[row * TS + 4 * ((sl >> 2) ^ (row & 7)) + (sl & 3)];
       }
+      // this CTA's z slices of the units finished now are counted at the next pass (pend), when
+      // the fence before the count finds these writes long complete
+      if (Q.ncnt && fin) pend = (int)(Q.nrows[G.unit[slot]] >> 7);
       if (pdec) {
         const long long tdec2 = clock64();
         prof[11] += tdec1 - tdec0;
@@ -1010,6 +1030,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     ++npass;
     if (!any) break;
   }
+  if (pend >= 0) {  // the last pass's notifications
+    __threadfence();
+    atomicAdd(&Q.ncnt[pend], 1u);
+  }
   if (prof != nullptr && gtid == 0 && crank == 0) {  // pass-count spread over the groups (tail)
     atomicMax(reinterpret_cast<unsigned long long*>(&prof[16]), (unsigned long long)npass);
     atomicAdd(reinterpret_cast<unsigned long long*>(&prof[17]), (unsigned long long)npass);
@@ -1024,9 +1048,11 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
 }
 
 // per-unit ||x||_inf; outputs of dead units (scale 0) and of max_iter <= 0 (l1reg.py:74-75,130-135)
+// (with a notification target, units finished here count as the P.cluster slices of the main kernel)
 __global__ void unit_scale_kernel(const float* __restrict__ X, Params P, float* __restrict__ scale, float* __restrict__ Z,
                                   float* __restrict__ E, int32_t* __restrict__ iters, float* __restrict__ res,
-                                  uint8_t* __restrict__ status) {
+                                  uint8_t* __restrict__ status, const int64_t* __restrict__ nrows = nullptr,
+                                  unsigned* ncnt = nullptr) {
   const int lane = threadIdx.x % 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t u = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < P.n_units; u += warps) {
@@ -1044,6 +1070,14 @@ __global__ void unit_scale_kernel(const float* __restrict__ X, Params P, float* 
         if (iters) iters[u] = dead ? 0 : P.max_iter;
         if (res) res[u] = dead ? 0.f : Limits<float>::inf();
         if (status) status[u] = dead ? L1F_UNIT_ZERO : L1F_UNIT_MAXITER;
+      }
+      if (ncnt) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(&ncnt[nrows[u] >> 7], (unsigned)P.cluster);
+        }
       }
     }
   }
@@ -1088,9 +1122,13 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
   P.tol = tol; P.rho = rho; P.beta0 = beta0; P.beta_max = beta_max;
   float* scale = (float*)workspace;
   int rc = L1F_OK;
-  unit_scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_units, 8), 65535), 256, 0, st>>>(X, P, scale, Z, E, iters,
-                                                                                              res, status);
+  NotifyHost* nh = g_notify;
+  g_notify = nullptr;
+  if (nh) nh->cluster = C;
+  unit_scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_units, 8), 65535), 256, 0, st>>>(
+      X, P, scale, Z, E, iters, res, status, nh ? nh->rows : nullptr, nh ? nh->cnt : nullptr);
   if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+  if (rc == L1F_OK && nh && nh->after_prologue && cudaEventRecord(nh->after_prologue, st) != cudaSuccess) rc = L1F_ERR_CUDA;
   if (rc == L1F_OK && max_iter > 0) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1117,6 +1155,12 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
       memset(prof, 0, 24 * sizeof(long long));
     }
     Pair Q = {};
+    if (nh) {
+      Q.nrows = nh->rows;
+      Q.ncnt = nh->cnt;
+      Q.nres = nh->resident;
+      nh->ctas = nclusters * C;
+    }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, A, lda, (const float*)scale, P, Lo, Z, E, iters, res, status, prof,
                                        Q);
     if (prof) {
@@ -1189,6 +1233,10 @@ int launch_pair(const float* X, int64_t ldx, int s, int64_t n_units, const float
                      passes((double)n2, (double)std::min<int64_t>(max_clusters, std::max<int64_t>(1, want2)));
   const double one = std::max(passes((double)n1, nc0), passes((double)n2, total - nc0));
   const bool paired = n1 > 0 && n2 > 0 && max_iter > 0 && total >= 2 && two.mode != 2 && (two.mode == 1 || one < seq);
+  if (two.mode == 3) {
+    *two.plan_out = paired ? 1 : 0;
+    return L1F_OK;
+  }
   if (!paired) {
     int rc = launch<KP, NG, NA, TA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, nullptr,
                                     s, iters, res, status, nullptr, 0, st, false, nullptr);
@@ -1214,7 +1262,7 @@ int launch_pair(const float* X, int64_t ldx, int s, int64_t n_units, const float
                                                                                          two.iters, two.res, two.status);
   if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
   if (rc == L1F_OK) {
-    Pair Q;
+    Pair Q = {};
     Q.X = two.X; Q.A = two.A; Q.lda = two.lda; Q.scale = scale2;
     Q.n_units = n2; Q.ldx = two.ldx; Q.ldz = two.ldz;
     Q.Z = two.Z; Q.iters = two.iters; Q.res = two.res; Q.status = two.status;

@@ -19,6 +19,7 @@
 // epilogue of tile t; four operand stages overlap loads and MMAs.  Edges are handled by TMA (zero
 // fill on load, clipping on store).  12 B of DRAM traffic per output entry.
 #include "common.cuh"
+#include "filter_pair.cuh"
 
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -321,6 +322,485 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant_
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------------------------
+// Streamed reconstruction (l1f_rowfilter_reconstruct_f32): the same tile pipeline, fed with work
+// items claimed at run time instead of a static raster, so that it can run BESIDE the row filter
+// on the SMs the filter's clusters leave free and consume its rows as they finish.
+//
+// A work item is (row strip s of 128 rows, CW consecutive column tiles); items are claimed in
+// strip-major order from a global counter.  Row strip s can be reconstructed once every row unit
+// of the strip has its z in global memory: the filter adds one per (unit, CTA of its cluster) to
+// ready[s] (filter_tc.cu, Pair::ncnt).  The CTA that claims chunk 0 of a strip builds the strip's
+// Af rows exactly as l1f_build_factors does (U row for a seed row, Zr row / sigma otherwise),
+// splits them into the fp16 pieces of split_factor_kernel (bitwise the same L as l1f_reconstruct)
+// and publishes split_flag[s]; the other chunks of the strip wait for that flag.  The producer
+// warp hands items to the MMA warp and the epilogue through a small shared-memory ring.
+constexpr int IR = 4;  // item ring entries
+
+struct StreamArgs {
+  unsigned* item_ctr;        // next work item (zero at the start of the call)
+  const unsigned* ready;     // per strip: notifications from the filter
+  unsigned* split_flag;      // per strip: its A pieces are in global memory
+  const int* skip;           // concurrent launch: nonzero = the gate timed out, do nothing
+  int* err;                  // a bounded wait timed out (residual -> NaN)
+  unsigned* split_ctr;        // next strip to split
+  int ntm;                    // strips
+  unsigned long long* dbg;   // L1F_RECON_DEBUG: [launch][items, first claim, last item done, split ns, ready-wait ns,
+                             //                   strips split, flag-wait ns]
+  int launch_id;
+  int cluster;               // notifications per row unit
+  const int64_t* row_idx;    // sorted seed rows (s_r)
+  const int* strip_p0;       // per strip s: lower_bound(row_idx, 128 s); ntm + 1 entries
+  const double* U;           // seed U (s_r x k, row-major)
+  const double* sigma;       // seed sigma (k)
+  const float* Zr;           // row-filter z, unit-major
+  int64_t ldzr;
+  int k, kp;
+  __half* ah;
+  __half* al;
+  float* inv_a;              // 2^-e of every Af row (written here)
+  int ipr, cw, n_items;      // items per strip, tiles per item, items
+};
+
+struct ItemRing {
+  int s[IR], tn0[IR], cnt[IR], w[IR];
+  unsigned long long full[IR], empty[IR];
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// bounded wait for *p >= need (a safety net: a wait that cannot end is a bug; after 10 s it
+// gives up and raises *err, which turns the residual into NaN instead of hanging the GPU)
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned need, int* err, unsigned sleep_ns) {
+  if (ld_acquire(p) >= need) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire(p) < need) {
+    if (globaltimer() - t0 > 10ull * 1000 * 1000 * 1000) { atomicExch(err, 1); return; }
+    __nanosleep(sleep_ns);
+  }
+}
+
+// Af rows of strip s (l1f_build_factors' formula) split into fp16 pieces (split_factor_kernel's
+// arithmetic), one warp, RB rows in flight per lane
+// Af rows of strip s built as l1f_build_factors does (U row for a seed row, Zr row times the
+// FP32-rounded reciprocal of sigma otherwise) and split into fp16 pieces with split_factor_kernel's
+// arithmetic (x 2^e by one multiply with an exact power of two, = ldexpf), so L is bitwise that
+// of the separate calls.  (FP64 arithmetic in this loop cost ~1000 cycles per value: measured.)  `nparts` warps share the strip (rows part, part + nparts, ...); a lane
+// owns column pairs t = 2 lane + 64 j, j < KJ2 (half2 stores).
+template <int KJ2>
+__device__ void split_rows(const StreamArgs& A, int s, int64_t m, int lane, int part, int nparts) {
+  constexpr int RB = KJ2 <= 2 ? 8 : 6;
+  constexpr int NV = 2 * KJ2;
+  const int k = A.k, kp = A.kp;
+  const int64_t ldz = A.ldzr;
+  const float* __restrict__ Zr = A.Zr;
+  const double* __restrict__ U = A.U;
+  const int64_t* __restrict__ ridx = A.row_idx;
+  __half* __restrict__ ah = A.ah;
+  __half* __restrict__ al = A.al;
+  float* __restrict__ inv = A.inv_a;
+  const int p0 = A.strip_p0[s], p1 = A.strip_p0[s + 1];
+  const int64_t i0 = (int64_t)s * BM, i1 = (i0 + BM < m ? i0 + (int64_t)BM : m);
+  const int nseed = p1 - p0;  // seed rows in the strip; lane q holds row_idx[p0 + q] (up to 32)
+  const int64_t my_seed = lane < nseed ? ridx[p0 + lane] : INT64_MAX;
+  float rsg[NV];  // 1 / sigma rounded to FP32 (l1f_build_factors' formula); no FP64 in the row loop
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int t = 2 * lane + 64 * (v >> 1) + (v & 1);
+    rsg[v] = t < k ? (float)(1.0 / A.sigma[t]) : 0.f;
+  }
+  for (int64_t ib = i0 + part; ib < i1; ib += (int64_t)RB * nparts) {
+    int pr[RB];
+    bool sd[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int64_t i = ib + (int64_t)rr * nparts;
+      if (nseed <= 32) {  // p = p0 + #{seed rows of the strip < i}
+        pr[rr] = p0 + __popc(__ballot_sync(0xffffffffu, my_seed < i));
+        sd[rr] = __ballot_sync(0xffffffffu, my_seed == i) != 0u;
+      } else {
+        int p = p0;
+        while (p < p1 && ridx[p] < i) ++p;
+        pr[rr] = p;
+        sd[rr] = p < p1 && ridx[p] == i;
+      }
+    }
+    float x[RB][NV];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {  // all loads of the batch in flight, then the arithmetic
+      const int64_t i = ib + (int64_t)rr * nparts;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int t = 2 * lane + 64 * (v >> 1) + (v & 1);
+        x[rr][v] = (i < i1 && t < k && !sd[rr]) ? __ldcg(Zr + (i - pr[rr]) * ldz + t) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int64_t i = ib + (int64_t)rr * nparts;
+      float mx = 0.f;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int t = 2 * lane + 64 * (v >> 1) + (v & 1);
+        float a = 0.f;
+        if (i < i1 && t < k) a = sd[rr] ? (float)U[(int64_t)pr[rr] * k + t] : x[rr][v] * rsg[v];
+        x[rr][v] = a;
+        mx = fmaxf(mx, fabsf(a));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (i >= i1) continue;
+      int ex = 0;
+      if (mx > 0.f) frexpf(mx, &ex);
+      const int e = mx > 0.f ? kScaleExp - ex : 0;
+      // x 2^e: one FP32 multiply by an exact power of two (= ldexpf) when 2^e is a normal float
+      const bool direct = e >= -126 && e <= 127;
+      const float two_e = __int_as_float((127 + (direct ? e : 0)) << 23);
+#pragma unroll
+      for (int j = 0; j < KJ2; ++j) {
+        const int t = 2 * lane + 64 * j;
+        if (t < kp) {
+          const float v0 = direct ? x[rr][2 * j] * two_e : ldexpf(x[rr][2 * j], e);
+          const float v1 = direct ? x[rr][2 * j + 1] * two_e : ldexpf(x[rr][2 * j + 1], e);
+          const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+          *reinterpret_cast<__half2*>(ah + i * kp + t) = __halves2half2(h0, h1);
+          *reinterpret_cast<__half2*>(al + i * kp + t) =
+              __halves2half2(__float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
+        }
+      }
+      if (lane == 0) inv[i] = ldexpf(1.f, -e);
+    }
+  }
+}
+
+// L1F_RECON_DEBUG=2: split_rows alone, two warps per strip (timing probe)
+template <int KJ2>
+__global__ void split_probe_kernel(StreamArgs A, int64_t m, unsigned long long* ns) {
+  const unsigned long long t0 = globaltimer();
+  split_rows<KJ2>(A, blockIdx.x, m, threadIdx.x % 32, threadIdx.x / 32, 2);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(ns, globaltimer() - t0);
+}
+
+template <int STAGES, int NMB, int KJ2>
+__global__ void __launch_bounds__(NTHREADS, 1)
+recon_stream_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                    const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
+                    const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmL,
+                    const __grid_constant__ CUtensorMap tmS, const float* __restrict__ inv_b, int64_t m, int64_t n,
+                    int kchunks, int ntn, StreamArgs SA, double* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  constexpr int MPF = NMB - 2;
+  using SmemT = Smem<STAGES, NMB>;
+  SmemT& sm = *reinterpret_cast<SmemT*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ ItemRing ring;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (SA.skip && *(volatile const int*)SA.skip) return;  // uniform: the whole CTA leaves
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], EPI); }
+    for (int b = 0; b < NMB; ++b) mbar_init(&sm.mfull[b], 1);
+    for (int r = 0; r < IR; ++r) { mbar_init(&ring.full[r], 1); mbar_init(&ring.empty[r], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ================= item claims, strip splits, TMA producer (lane 0 issues)
+    int it = 0;
+    for (int ni = 0;; ++ni) {
+      const int r = ni % IR;
+      int w = 0;
+      if (lane == 0) {
+        mbar_wait(&ring.empty[r], ((ni / IR) & 1) ^ 1);
+        w = (int)atomicAdd(SA.item_ctr, 1u);
+      }
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= SA.n_items) {
+        if (lane == 0) { ring.cnt[r] = 0; mbar_arrive(&ring.full[r]); }
+        break;
+      }
+      unsigned long long* dbg = SA.dbg ? SA.dbg + 8 * SA.launch_id : nullptr;
+      const unsigned long long tw0 = dbg ? globaltimer() : 0ull;
+      if (dbg && lane == 0) { atomicAdd(dbg, 1ull); atomicMin(dbg + 1, tw0); }
+      const int s = w / SA.ipr, c = w - s * SA.ipr;
+      if (lane == 0) {  // the strip's A pieces (split by the splitter warps of some CTA)
+        wait_geq(SA.split_flag + s, 1u, SA.err, 128);
+        fence_async_global();
+        if (dbg) atomicAdd(dbg + 6, globaltimer() - tw0);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int tn0 = c * SA.cw, cnt = min(SA.cw, ntn - tn0);
+        ring.s[r] = s; ring.tn0[r] = tn0; ring.cnt[r] = cnt; ring.w[r] = w;
+        mbar_arrive(&ring.full[r]);
+        for (int j = 0; j < cnt; ++j) {
+          for (int kc = 0; kc < kchunks; ++kc, ++it) {
+            const int st = it % STAGES, ph = (it / STAGES) & 1;
+            mbar_wait(&sm.empty[st], ph ^ 1);
+            mbar_expect_arrive(&sm.full[st], 4 * OP_BYTES);
+            tma_load(sm.a_hi[st], &tmAh, kc * BK, s * BM, &sm.full[st]);
+            tma_load(sm.b_hi[st], &tmBh, kc * BK, (tn0 + j) * BN, &sm.full[st]);
+            tma_load(sm.a_lo[st], &tmAl, kc * BK, s * BM, &sm.full[st]);
+            tma_load(sm.b_lo[st], &tmBl, kc * BK, (tn0 + j) * BN, &sm.full[st]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    int it = 0, ti = 0;
+    for (int ni = 0;; ++ni) {
+      const int r = ni % IR;
+      mbar_wait(&ring.full[r], (ni / IR) & 1);
+      const int cnt = ring.cnt[r];
+      if (cnt == 0) break;
+      for (int j = 0; j < cnt; ++j, ++ti) {
+        const int acc = ti & 1, aph = (ti >> 1) & 1;
+        mbar_wait(&sm.tempty[acc], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const int st = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&sm.full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            const uint32_t ah = sa(sm.a_hi[st]), bh = sa(sm.b_hi[st]), al = sa(sm.a_lo[st]), bl = sa(sm.b_lo[st]);
+#pragma unroll
+            for (int jj = 0; jj < BK / 16; ++jj) {
+              const uint32_t off = 32u * jj;
+              mma_f16(d, smem_desc(ah + off), smem_desc(bh + off), (kc | jj) ? 1u : 0u);
+              mma_f16(d, smem_desc(ah + off), smem_desc(bl + off), 1u);
+              mma_f16(d, smem_desc(al + off), smem_desc(bh + off), 1u);
+            }
+            mma_commit(&sm.empty[st]);
+            if (kc == kchunks - 1) mma_commit(&sm.tfull[acc]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ================= splitters: claim strips, wait until their row units are done, build and
+    // split their Af rows, publish split_flag (strips are claimed in order, ahead of the tiles)
+    __shared__ int split_s;
+    for (;;) {
+      if (warp == 2 && lane == 0) {
+        const int s = (int)atomicAdd(SA.split_ctr, 1u);
+        split_s = s;
+        if (s < SA.ntm) {
+          const int64_t rows = m - (int64_t)s * BM < BM ? m - (int64_t)s * BM : (int64_t)BM;
+          const unsigned need = (unsigned)SA.cluster * (unsigned)(rows - (SA.strip_p0[s + 1] - SA.strip_p0[s]));
+          const unsigned long long tw = SA.dbg ? globaltimer() : 0ull;
+          wait_geq(SA.ready + s, need, SA.err, 256);
+          if (SA.dbg) atomicAdd(SA.dbg + 8 * SA.launch_id + 4, globaltimer() - tw);
+        }
+      }
+      named_bar(2, 64);
+      const int s = *(volatile int*)&split_s;
+      if (s >= SA.ntm) break;
+      const unsigned long long ts0 = SA.dbg ? globaltimer() : 0ull;
+      split_rows<KJ2>(SA, s, m, lane, warp - 2, 2);
+      fence_async_global();
+      __threadfence();
+      named_bar(2, 64);
+      if (warp == 2 && lane == 0) {
+        st_release(SA.split_flag + s, 1u);
+        if (SA.dbg) {
+          atomicAdd(SA.dbg + 8 * SA.launch_id + 3, globaltimer() - ts0);
+          atomicAdd(SA.dbg + 8 * SA.launch_id + 5, 1ull);
+        }
+      }
+    }
+  } else if (warp >= EPI0) {
+    // ================= epilogue (as recon_tc_kernel; tiles from the item ring)
+    const int ew = warp - EPI0, q = warp & 3, half = ew >> 2;
+    const int row = 32 * q + lane;
+    const bool leader = threadIdx.x == 32 * EPI0;
+    double m2 = 0.0;
+    int ti = 0, g = 0;
+    // look-ahead cursor over the chunk sequence (leader only): M prefetch coordinates
+    int la_n = 0, la_j = 0, la_cc = 0, la_cnt = 0, la_s = 0, la_tn0 = 0;
+    bool la_end = false;
+    auto la_next = [&](int& x, int& y) -> bool {
+      if (la_end) return false;
+      if (la_j == la_cnt) {
+        const int r = la_n % IR;
+        mbar_wait(&ring.full[r], (la_n / IR) & 1);
+        la_cnt = ring.cnt[r]; la_s = ring.s[r]; la_tn0 = ring.tn0[r];
+        la_j = 0; la_cc = 0;
+        ++la_n;
+        if (la_cnt == 0) { la_end = true; return false; }
+      }
+      x = (la_tn0 + la_j) * BN + la_cc * 32;
+      y = la_s * BM;
+      if (++la_cc == BN / 32) { la_cc = 0; ++la_j; }
+      return true;
+    };
+    int pf = 0;  // chunks whose M load was issued
+    if (leader) {
+      for (; pf < MPF; ++pf) {
+        int x, y;
+        if (!la_next(x, y)) break;
+        mbar_expect_arrive(&sm.mfull[pf % NMB], CHUNK_BYTES);
+        tma_load(sm.mbuf[pf % NMB], &tmM, x, y, &sm.mfull[pf % NMB]);
+      }
+    }
+    for (int ni = 0;; ++ni) {
+      const int r = ni % IR;
+      mbar_wait(&ring.full[r], (ni / IR) & 1);
+      const int cnt = ring.cnt[r], tm = ring.s[r], tn0 = ring.tn0[r], w = ring.w[r];
+      if (cnt == 0) break;
+      const int64_t gi = (int64_t)tm * BM + row;
+      const float sca = gi < m ? __ldcg(SA.inv_a + gi) : 0.f;  // written in this launch (split_strip)
+      for (int j = 0; j < cnt; ++j, ++ti) {
+        const int tn = tn0 + j;
+        const int acc = ti & 1, aph = (ti >> 1) & 1;
+        {
+          const int et = threadIdx.x - 32 * EPI0;
+          const int64_t gj = (int64_t)tn * BN + et;
+          if (et < BN) sm.colscale[ti & 1][et] = gj < n ? inv_b[gj] : 0.f;
+        }
+        mbar_wait(&sm.tfull[acc], aph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int cc = 0; cc < BN / 32; ++cc, ++g) {
+          const int mb = g % NMB, lb = g & 1;
+          uint32_t v[16];
+          const uint32_t taddr = tmem + (uint32_t)(acc * BN + cc * 32 + 16 * half) + ((uint32_t)(32 * q) << 16);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (cc == BN / 32 - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&sm.tempty[acc]);
+          }
+          if (leader) {
+            tma_wait_read1();
+            int x, y;
+            if (pf == g + MPF && la_next(x, y)) {  // M of chunk g + MPF into the buffer freed above
+              const int nb = pf % NMB;
+              mbar_expect_arrive(&sm.mfull[nb], CHUNK_BYTES);
+              tma_load(sm.mbuf[nb], &tmM, x, y, &sm.mfull[nb]);
+              ++pf;
+            }
+          }
+          mbar_wait(&sm.mfull[mb], (g / NMB) & 1);
+          named_bar(1, EPI);
+          float4* mrow = reinterpret_cast<float4*>(sm.mbuf[mb] + row * 128);
+          float4* lrow = reinterpret_cast<float4*>(sm.lbuf[lb] + row * 128);
+          float macc = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int jq = 4 * half + jj, p = jq ^ (row & 7);
+            const float4 c4 = *reinterpret_cast<const float4*>(&sm.colscale[ti & 1][cc * 32 + 4 * jq]);
+            const float4 l4 = make_float4(__uint_as_float(v[4 * jj]) * sca * c4.x,
+                                          __uint_as_float(v[4 * jj + 1]) * sca * c4.y,
+                                          __uint_as_float(v[4 * jj + 2]) * sca * c4.z,
+                                          __uint_as_float(v[4 * jj + 3]) * sca * c4.w);
+            lrow[p] = l4;
+            const float4 m4 = mrow[p];
+            mrow[p] = make_float4(m4.x - l4.x, m4.y - l4.y, m4.z - l4.z, m4.w - l4.w);
+            macc = fmaf(m4.x, m4.x, fmaf(m4.y, m4.y, fmaf(m4.z, m4.z, fmaf(m4.w, m4.w, macc))));
+          }
+          m2 += (double)macc;
+          fence_async_smem();
+          named_bar(1, EPI);
+          if (leader) {
+            const int x = tn * BN + cc * 32, y = tm * BM;
+            tma_store(&tmL, x, y, sm.lbuf[lb]);
+            tma_store(&tmS, x, y, sm.mbuf[mb]);
+            tma_commit();
+          }
+        }
+      }
+      // per-item partial of sum M^2 (deterministic: fixed item boundaries, fixed order)
+      m2 = warp_sum(m2);
+      if (lane == 0) sm.red[1][ew] = m2;
+      named_bar(1, EPI);
+      if (leader) {
+        double c = 0;
+        for (int i = 0; i < 8; ++i) c += sm.red[1][i];
+        part[2 * (int64_t)w] = 0.0;
+        part[2 * (int64_t)w + 1] = c;
+        mbar_arrive(&ring.empty[r]);
+        if (SA.dbg) atomicMax(SA.dbg + 8 * SA.launch_id + 2, globaltimer());
+      }
+      m2 = 0.0;
+    }
+    if (leader) tma_wait_all();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// waits (one thread) until the filter's CTAs are all resident, so the concurrent reconstruction
+// only takes SMs the filter does not use; on timeout it tells that launch to do nothing
+__global__ void recon_gate_kernel(const unsigned* resident, unsigned need, int* skip, unsigned long long timeout_ns) {
+  if (threadIdx.x) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire(resident) < need) {
+    if (globaltimer() - t0 > timeout_ns) { *skip = 1; return; }
+    __nanosleep(500);
+  }
+}
+
+// deterministic sum of per-item (r2, m2) partials: fixed strided order per thread, fixed tree
+__global__ void sum_items_kernel(const double* __restrict__ part, int n, const int* err, double* __restrict__ out) {
+  __shared__ double ra[1024], rb[1024];
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { a += part[2 * i]; b += part[2 * i + 1]; }
+  ra[threadIdx.x] = a;
+  rb[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) { ra[threadIdx.x] += ra[threadIdx.x + w]; rb[threadIdx.x] += rb[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const bool bad = err && *err;
+    out[0] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ra[0];
+    out[1] = rb[0];
+  }
+}
+
+__global__ void strip_p0_kernel(const int64_t* __restrict__ row_idx, int64_t s_r, int nstrips, int* __restrict__ p0) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= nstrips; s += gridDim.x * blockDim.x) {
+    const int64_t key = (int64_t)s * BM;
+    int64_t lo = 0, hi = s_r;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (row_idx[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    p0[s] = (int)lo;
+  }
+}
+
 // two-piece FP16 split of a rows x k factor into rows x kp (kp % 32 == 0, zero padded): one warp
 // per row; x 2^e = h + l with max |x| 2^e in [2^13, 2^14), inv[row] = 2^-e (1 for a zero row)
 __global__ void split_factor_kernel(const float* __restrict__ src, int64_t rows, int k, int64_t lds, int kp,
@@ -457,5 +937,263 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
   cudaFreeAsync(bh, st);
   cudaFreeAsync(ia, st);
   cudaFreeAsync(part, st);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Row filter + reconstruction, overlapped (see recon_stream_kernel above).
+int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
+                    double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
+                    float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
+                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+
+namespace {
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+};
+SideStream* side_stream() {  // one per device, created on first use
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  SideStream& s = per_dev[dev];
+  if (!s.st) {
+    if (cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.e0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.e1, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.e2, cudaEventDisableTiming) != cudaSuccess) {
+      s.st = nullptr;
+      return nullptr;
+    }
+  }
+  return &s;
+}
+}  // namespace
+
+extern "C" int l1f_rowfilter_reconstruct_f32(
+    const float* Xr, int64_t ldx, int32_t s, int64_t n_units, const float* V, int64_t ldv, int32_t k, float tol,
+    float rho, float beta0, float beta_max, int32_t max_iter, float* Zr, int64_t ldz, int32_t* iters, float* res,
+    uint8_t* status, const int64_t* unit_rows, const int64_t* row_idx, int64_t s_r, const double* U,
+    const double* sigma, const int64_t* col_idx, int64_t s_c, const double* V64, const float* Zc, int64_t ldzc,
+    const float* M, int64_t m, int64_t n, int64_t ldm, float* L,
+    int64_t ldl, float* S, int64_t lds, double* resid_sq, void* ev_filter_done, void* stream) {
+  using namespace l1f;
+  using namespace l1f::rtc;
+  L1F_REQUIRE(m >= 1 && n >= 1 && k >= 1 && s >= 1 && s_r >= 0 && s_r <= m && n_units == m - s_r, L1F_ERR_ARG,
+              "rowfilter_reconstruct: need the m - s_r non-seed rows as units");
+  L1F_REQUIRE(ldx >= s && ldz >= k && ldv >= k && ldzc >= k && ldm >= n && ldl >= n && lds >= n && s_c >= 0 && s_c <= n,
+              L1F_ERR_ARG,
+              "rowfilter_reconstruct: leading dimension too small");
+  L1F_REQUIRE(M && L && S && Zr && (s_r == 0 || (U && row_idx)) && (s_c == 0 || (V64 && col_idx)) && sigma &&
+                  (s_c == n || Zc),
+              L1F_ERR_ARG,
+              "rowfilter_reconstruct: null operand");
+  const char* env = getenv("L1F_RECON_STREAM");
+  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  const char* tce = getenv("L1F_RECON_TC");
+  if (tce && tce[0] == '0') return L1F_ERR_UNSUPPORTED;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  if (k <= 16 || k > 224 || !al16(M) || !al16(L) || !al16(S) || ldm % 4 || ldl % 4 || lds % 4 ||
+      m >= INT32_MAX / 2 || n >= INT32_MAX / 2 || !encode_fn())
+    return L1F_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  SideStream* side = side_stream();
+  if (!side) return L1F_ERR_UNSUPPORTED;
+  const int kp = (int)ceil_div(k, BK) * BK;
+  const int KJ2 = (int)ceil_div(kp, 64);
+  const int ntm = (int)ceil_div(m, BM), ntn = (int)ceil_div(n, BN);
+  const int cw = 16;
+  const int ipr = (int)ceil_div(ntn, cw);
+  const int64_t n_items64 = (int64_t)ntm * ipr;
+  L1F_REQUIRE(n_items64 < INT32_MAX / 2, L1F_ERR_UNSUPPORTED, "rowfilter_reconstruct: too many tiles");
+  const int n_items = (int)n_items64;
+  // scratch: A and B pieces, row / column scales, per-item partials, counters
+  __half *ah = nullptr, *bh = nullptr;
+  float* ia = nullptr;
+  double* part = nullptr;
+  unsigned* ctr = nullptr;
+  const int64_t m4 = ceil_div(m, 4) * 4;
+  L1F_CUDA_TRY(cudaMallocAsync(&ah, sizeof(__half) * (size_t)m * kp * 2, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&bh, sizeof(__half) * (size_t)n * kp * 2, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&ia, sizeof(float) * ((size_t)(m4 + n) + (size_t)n * k), st));
+  L1F_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * 2 * (size_t)n_items, st));
+  // counters: item_ctr, resident, skip, err, split_ctr, pad x 3 | ready[ntm] | split_flag[ntm] | strip_p0[ntm + 1]
+  const size_t n_ctr = 8 + 3 * (size_t)ntm + 1;
+  L1F_CUDA_TRY(cudaMallocAsync(&ctr, sizeof(unsigned) * n_ctr, st));
+  __half* al = ah + (size_t)m * kp;
+  __half* bl = bh + (size_t)n * kp;
+  float* ib = ia + m4;
+  float* bf = ib + n;  // Bf (n x k), built here from Zc and the seed's V, sigma
+  unsigned* item_ctr = ctr;
+  unsigned* resident = ctr + 1;
+  int* skip = reinterpret_cast<int*>(ctr + 2);
+  unsigned* split_ctr = ctr + 4;
+  unsigned* ready = ctr + 8;
+  unsigned* split_flag = ready + ntm;
+  int* strip_p0 = reinterpret_cast<int*>(split_flag + ntm);
+  int rc = L1F_OK;
+  const int nsm = num_sms();
+  CUtensorMap tAh, tAl, tBh, tBl, tM, tL, tS;
+  const auto W = CU_TENSOR_MAP_SWIZZLE_128B, W64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  bool ok = make_map(&tAh, ah, m, kp, kp, BK, W64, true) && make_map(&tAl, al, m, kp, kp, BK, W64, true) &&
+            make_map(&tBh, bh, n, kp, kp, BK, W64, true) && make_map(&tBl, bl, n, kp, kp, BK, W64, true) &&
+            make_map(&tM, M, m, n, ldm, 32, W) && make_map(&tL, L, m, n, ldl, 32, W) && make_map(&tS, S, m, n, lds, 32, W);
+  if (!ok) {
+    set_error("rowfilter_reconstruct: cuTensorMapEncodeTiled failed");
+    rc = L1F_ERR_UNSUPPORTED;
+  }
+  if (rc == L1F_OK && cudaMemsetAsync(ctr, 0, sizeof(unsigned) * n_ctr, st) != cudaSuccess) rc = L1F_ERR_CUDA;
+  // the reconstruction's prologue (Bf, its pieces, the strips' seed-row offsets) is not needed by
+  // the row filter: it runs on the side stream, on the SMs the filter leaves free
+  auto prologue = [&](cudaStream_t q) -> int {
+    const char* sy = getenv("L1F_RECON_SYNC");
+    auto chk = [&](const char* what) {
+      if (sy && sy[0] == '1') {
+        cudaError_t e = cudaStreamSynchronize(q);
+        fprintf(stderr, "[recon sync] %s: %s\n", what, cudaGetErrorString(e));
+      }
+    };
+    chk("before prologue");
+    int r = l1f_build_factors(L1F_F32, 0, n, k, nullptr, 0, col_idx, s_c, nullptr, sigma, V64, Zc, ldzc, nullptr, k,
+                              nullptr, bf, q);
+    if (r != L1F_OK) return r;
+    chk("build_factors");
+    strip_p0_kernel<<<(unsigned)ceil_div(ntm + 1, 256), 256, 0, q>>>(row_idx, s_r, ntm, strip_p0);
+    chk("strip_p0");
+    split_factor_kernel<<<nsm * 4, 256, 0, q>>>(bf, n, k, k, kp, bh, bl, ib);
+    chk("split B");
+    return cudaGetLastError() == cudaSuccess ? L1F_OK : L1F_ERR_CUDA;
+  };
+  // the row filter, counting finished units per strip
+  tcf::NotifyHost nh;
+  if (rc == L1F_OK) {
+    nh.rows = unit_rows;
+    nh.cnt = ready;
+    nh.resident = resident;
+    nh.after_prologue = side->e0;
+    tcf::g_notify = &nh;
+    rc = l1f_tc_dispatch(Xr, ldx, s, n_units, V, ldv, k, tol, rho, beta0, beta_max, max_iter, Zr, ldz, nullptr, s, iters,
+                         res, status, nullptr, 0, st, false, nullptr);
+    tcf::g_notify = nullptr;
+    if (rc == L1F_OK && nh.cluster == 0) rc = L1F_ERR_UNSUPPORTED;  // the tensor-core launch did not run
+  }
+  if (rc == L1F_OK && ev_filter_done && cudaEventRecord((cudaEvent_t)ev_filter_done, st) != cudaSuccess) rc = L1F_ERR_CUDA;
+  if (rc == L1F_OK) {
+    const bool mid = kp <= 128;
+    const size_t smem = (mid ? sizeof(Smem<3, 6>) : sizeof(Smem<4, 4>)) + 1024;
+    StreamArgs SA;
+    SA.item_ctr = item_ctr; SA.ready = ready; SA.split_flag = split_flag; SA.skip = nullptr;
+    SA.err = reinterpret_cast<int*>(ctr + 3);
+    SA.cluster = nh.cluster; SA.row_idx = row_idx; SA.strip_p0 = strip_p0; SA.U = U; SA.sigma = sigma;
+    SA.Zr = Zr; SA.ldzr = ldz; SA.k = k; SA.kp = kp; SA.ah = ah; SA.al = al; SA.inv_a = ia;
+    SA.ipr = ipr; SA.cw = cw; SA.n_items = n_items; SA.split_ctr = split_ctr; SA.ntm = ntm;
+    const char* dbe = getenv("L1F_RECON_DEBUG");
+    unsigned long long* dbg = nullptr;
+    if (dbe && dbe[0] == '1') {
+      cudaMallocManaged(&dbg, sizeof(unsigned long long) * 16);
+      for (int i = 0; i < 16; ++i) dbg[i] = (i % 8 == 1) ? ~0ull : 0ull;
+      cudaStreamSynchronize(st);
+    }
+    SA.dbg = dbg;
+    int next_id = 0;
+    auto launch = [&](auto kern, int grid, cudaStream_t stream_, const int* skip_) -> bool {
+      static std::mutex mu;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }
+      StreamArgs a = SA;
+      a.skip = skip_;
+      a.launch_id = next_id++;
+      kern<<<grid, NTHREADS, smem, stream_>>>(tAh, tAl, tBh, tBl, tM, tL, tS, ib, m, n, kp / BK, ntn, a, part);
+      return cudaGetLastError() == cudaSuccess;
+    };
+    auto launch_kj = [&](int grid, cudaStream_t stream_, const int* skip_) -> bool {
+      switch (KJ2) {
+        case 1: return launch(recon_stream_kernel<3, 6, 1>, grid, stream_, skip_);
+        case 2: return launch(recon_stream_kernel<3, 6, 2>, grid, stream_, skip_);
+        case 3: return launch(recon_stream_kernel<4, 4, 3>, grid, stream_, skip_);
+        case 4: return launch(recon_stream_kernel<4, 4, 4>, grid, stream_, skip_);
+      }
+      return false;
+    };
+    (void)mid;
+    if (dbe && dbe[0] == '2') {
+      unsigned long long* ns = nullptr;
+      cudaMallocManaged(&ns, sizeof(unsigned long long));
+      *ns = 0;
+      cudaStreamSynchronize(st);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+      switch (KJ2) {
+        case 1: split_probe_kernel<1><<<ntm, 64, 0, st>>>(SA, m, ns); break;
+        case 2: split_probe_kernel<2><<<ntm, 64, 0, st>>>(SA, m, ns); break;
+        case 3: split_probe_kernel<3><<<ntm, 64, 0, st>>>(SA, m, ns); break;
+        case 4: split_probe_kernel<4><<<ntm, 64, 0, st>>>(SA, m, ns); break;
+      }
+      cudaEventRecord(b, st);
+      cudaStreamSynchronize(st);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      fprintf(stderr, "[split probe] %d strips, kernel %.3f ms, %.1f us per strip (two warps each)\n", ntm, ms,
+              (double)*ns / 1e3 / ntm);
+      cudaFree(ns);
+    }
+    // concurrent part on the SMs the filter leaves free, after the filter is fully resident
+    const int spare = nh.ctas > 0 ? nsm - nh.ctas : 0;
+    const char* ce = getenv("L1F_RECON_CONCURRENT");
+    const bool concurrent = spare > 0 && !(ce && ce[0] == '0');
+    if (concurrent) {
+      if (cudaStreamWaitEvent(side->st, side->e0, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+      if (rc == L1F_OK) {
+        recon_gate_kernel<<<1, 32, 0, side->st>>>(resident, (unsigned)nh.ctas, skip, 1000ull * 1000);
+        if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+      }
+      if (rc == L1F_OK) rc = prologue(side->st);
+      if (rc == L1F_OK && (cudaEventRecord(side->e2, side->st) != cudaSuccess ||
+                           !launch_kj(std::min(spare, n_items), side->st, skip) ||
+                           cudaEventRecord(side->e1, side->st) != cudaSuccess))
+        rc = L1F_ERR_CUDA;
+      if (rc == L1F_OK && cudaStreamWaitEvent(st, side->e2, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+    } else if (rc == L1F_OK) {
+      rc = prologue(st);
+    }
+    // the rest once the filter has finished, on every SM
+    if (rc == L1F_OK && !launch_kj(std::min(nsm, n_items), st, nullptr)) rc = L1F_ERR_CUDA;
+    if (concurrent && cudaStreamWaitEvent(st, side->e1, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+    if (rc == L1F_OK && resid_sq) {
+      sum_items_kernel<<<1, 1024, 0, st>>>(part, n_items, reinterpret_cast<const int*>(ctr + 3), resid_sq);
+      if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+    }
+    if (rc == L1F_ERR_CUDA) set_error("rowfilter_reconstruct: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (dbg) {
+      cudaDeviceSynchronize();
+      int skip_h = 0, err_h = 0;
+      cudaMemcpy(&skip_h, skip, sizeof(int), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&err_h, ctr + 3, sizeof(int), cudaMemcpyDeviceToHost);
+      const unsigned long long t0 = std::min(dbg[1], dbg[9]);
+      fprintf(stderr, "[recon stream] filter ctas %d cluster %d spare %d concurrent %d skip %d err %d items %d\n", nh.ctas,
+              nh.cluster, spare, (int)concurrent, skip_h, err_h, n_items);
+      for (int l = 0; l < next_id; ++l) {
+        const unsigned long long* d = dbg + 8 * l;
+        const double strips = std::max(1.0, (double)d[5]);
+        fprintf(stderr, "[recon stream] launch %d: items %llu, first claim +%.3f ms, last item done +%.3f ms; "
+                "strips split %llu, split %.1f us per strip, readiness wait %.1f us per strip; flag wait %.1f us per "
+                "item\n", l, d[0], d[0] ? (double)(d[1] - t0) * 1e-6 : 0.0, d[0] ? (double)(d[2] - t0) * 1e-6 : 0.0,
+                d[5], (double)d[3] / 1e3 / strips, (double)d[4] / 1e3 / strips,
+                d[0] ? (double)d[6] / 1e3 / (double)d[0] : 0.0);
+      }
+      cudaFree(dbg);
+    }
+  }
+  cudaFreeAsync(ah, st);
+  cudaFreeAsync(bh, st);
+  cudaFreeAsync(ia, st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(ctr, st);
   return rc;
 }
