@@ -77,6 +77,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes ~0.1-0.3 s to print its first sample: start timing only once it
+            # samples, so a short timed region still gets samples (the prior ones are dropped)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self

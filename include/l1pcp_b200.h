@@ -166,6 +166,22 @@ int l1f_rowfilter_reconstruct_f32(const float* X, int64_t ldx, int32_t s, int64_
                                   float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
                                   void* ev_filter_done, void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * A filter launch with an index gather beside it — filter_columns (l1filter.py:116-122) while
+ * the row panel m[np.ix_(comp_rows, col_idx)] (l1filter.py:243) is extracted: the filter as
+ * l1f_filter_f32 (no e output) and out = l1f_gather(dtype_in, M, ..., L1F_F32, out, ...), the
+ * gather on the SMs the filter's clusters leave free once they are all resident.  Both are
+ * complete when the stream reaches the next operation.  L1F_ERR_UNSUPPORTED (nothing launched)
+ * when the tensor-core filter does not apply; then call the two functions.
+ * ---------------------------------------------------------------------------------- */
+int l1f_filter_with_gather_f32(const float* X, int64_t ldx, int32_t s, int64_t n_units,
+                               const float* A, int64_t lda, int32_t k, float tol, float rho,
+                               float beta0, float beta_max, int32_t max_iter,
+                               float* Z, int64_t ldz, int32_t* iters, float* res, uint8_t* status,
+                               int32_t dtype_in, const void* M, int64_t ldm,
+                               const int64_t* rows, int64_t n_rows, const int64_t* cols, int64_t n_cols,
+                               float* out, int64_t ldo, int32_t transpose, void* stream);
+
 /* General C = alpha * A B^T (+ beta*C), A m x k, B n x k, row-major; used for the small
  * dense products of the reference API (SkinnySvd.reconstruct matcore.py:36-38,
  * pseudo_inverse_apply matcore.py:116-123, nystrom_complete_via_pinv l1filter.py:144-148). */

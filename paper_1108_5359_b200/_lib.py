@@ -72,6 +72,9 @@ SIGNATURES = {
                                              _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                                              _vp, _i64,
                                              _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "l1f_filter_with_gather_f32": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _i32,
+                                          _vp, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64,
+                                          _vp, _i64, _i32, _vp]),
     "l1f_gemm_nt": (_int, [_int, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _vp]),
     "l1f_generate_factors_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "l1f_generate_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _f32, _f32, _vp, _vp, _i64, _i64,

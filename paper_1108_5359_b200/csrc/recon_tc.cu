@@ -765,7 +765,10 @@ __global__ void recon_gate_kernel(const unsigned* resident, unsigned need, int* 
   if (threadIdx.x) return;
   const unsigned long long t0 = globaltimer();
   while (ld_acquire(resident) < need) {
-    if (globaltimer() - t0 > timeout_ns) { *skip = 1; return; }
+    if (globaltimer() - t0 > timeout_ns) {
+      if (skip) *skip = 1;
+      return;
+    }
     __nanosleep(500);
   }
 }
@@ -1195,5 +1198,56 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
   cudaFreeAsync(ia, st);
   cudaFreeAsync(part, st);
   cudaFreeAsync(ctr, st);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// A filter launch with an index gather beside it (the column filter and the row panel of the
+// pipeline): the gather runs on the SMs the filter's clusters leave free, once they are all
+// resident.  Results are exactly those of l1f_gather followed by l1f_filter_f32 (no e output).
+extern "C" int l1f_filter_with_gather_f32(const float* X, int64_t ldx, int32_t s, int64_t n_units, const float* A,
+                                          int64_t lda, int32_t k, float tol, float rho, float beta0, float beta_max,
+                                          int32_t max_iter, float* Z, int64_t ldz, int32_t* iters, float* res,
+                                          uint8_t* status, int32_t dtype_in, const void* M, int64_t ldm,
+                                          const int64_t* rows, int64_t n_rows, const int64_t* cols, int64_t n_cols,
+                                          float* out, int64_t ldo, int32_t transpose, void* stream) {
+  using namespace l1f;
+  using namespace l1f::rtc;
+  L1F_REQUIRE(s >= 1 && k >= 1 && n_units >= 0 && ldx >= s && ldz >= k && lda >= k, L1F_ERR_ARG,
+              "filter_with_gather: bad filter shape");
+  const char* env = getenv("L1F_GATHER_OVERLAP");
+  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  SideStream* side = side_stream();
+  if (!side || n_units == 0 || max_iter <= 0) return L1F_ERR_UNSUPPORTED;
+  unsigned* resident = nullptr;
+  L1F_CUDA_TRY(cudaMallocAsync(&resident, sizeof(unsigned), st));
+  int rc = cudaMemsetAsync(resident, 0, sizeof(unsigned), st) == cudaSuccess ? L1F_OK : L1F_ERR_CUDA;
+  tcf::NotifyHost nh;
+  if (rc == L1F_OK) {
+    nh.resident = resident;
+    nh.after_prologue = side->e0;
+    tcf::g_notify = &nh;
+    rc = l1f_tc_dispatch(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, nullptr, s, iters,
+                         res, status, nullptr, 0, st, false, nullptr);
+    tcf::g_notify = nullptr;
+    if (rc == L1F_OK && nh.ctas == 0) rc = L1F_ERR_UNSUPPORTED;
+  }
+  if (rc == L1F_OK) {
+    const int spare = num_sms() - nh.ctas;
+    if (spare > 0) {
+      if (cudaStreamWaitEvent(side->st, side->e0, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+      if (rc == L1F_OK) {  // on a gate timeout the gather runs anyway (only its placement is at stake)
+        recon_gate_kernel<<<1, 32, 0, side->st>>>(resident, (unsigned)nh.ctas, nullptr, 1000ull * 1000);
+        rc = l1f_gather(dtype_in, M, ldm, rows, n_rows, cols, n_cols, L1F_F32, out, ldo, transpose, side->st);
+        if (rc == L1F_OK && (cudaEventRecord(side->e1, side->st) != cudaSuccess ||
+                             cudaStreamWaitEvent(st, side->e1, 0) != cudaSuccess))
+          rc = L1F_ERR_CUDA;
+      }
+    } else {
+      rc = l1f_gather(dtype_in, M, ldm, rows, n_rows, cols, n_cols, L1F_F32, out, ldo, transpose, st);
+    }
+  }
+  cudaFreeAsync(resident, st);
   return rc;
 }

@@ -333,11 +333,27 @@ def solve_step(plan, mt, l_out=None, s_out=None, events=None):
     _lib.call("l1f_gather", _lib.F32, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx), len(seed.row_idx),
               dv.ptr(plan.d_comp_cols), len(plan.comp_cols), _lib.F32, dv.ptr(xc), xc.stride(0), 1, dv.stream())
     xr = torch.empty((len(plan.comp_rows), len(seed.col_idx)), dtype=torch.float32, device="cuda")
-    _lib.call("l1f_gather", _lib.F32, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local), len(plan.comp_rows),
-              dv.ptr(plan.d_col_idx), len(seed.col_idx), _lib.F32, dv.ptr(xr), xr.stride(0), 0, dv.stream())
     if events is not None:
         events[1].record()
-    zc, _, itc, rc, stc = filter_units(xc, plan.u, adm, want_e=False, workspace=plan.workspace)
+    # column filter, with the row panel gathered beside it on the SMs its clusters leave free
+    nc = len(plan.comp_cols)
+    zc = torch.empty((nc, k), dtype=torch.float32, device="cuda")
+    itc = torch.empty(nc, dtype=torch.int32, device="cuda")
+    rc = torch.empty(nc, dtype=torch.float32, device="cuda")
+    stc = torch.empty(nc, dtype=torch.uint8, device="cuda")
+    beta0 = float(adm.beta0) if adm.beta0 is not None else 0.0
+    beta_max = float(adm.beta_max) if adm.beta_max is not None else 0.0
+    gather_args = (_lib.F32, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local), len(plan.comp_rows),
+                   dv.ptr(plan.d_col_idx), len(seed.col_idx), dv.ptr(xr), xr.stride(0), 0)
+    code = _lib.load().l1f_filter_with_gather_f32(
+        dv.ptr(xc), xc.stride(0), len(seed.row_idx), nc, dv.ptr(plan.u), plan.u.stride(0), k, float(adm.tol),
+        float(adm.rho), beta0, beta_max, int(adm.max_iter), dv.ptr(zc), zc.stride(0), dv.ptr(itc), dv.ptr(rc),
+        dv.ptr(stc), *gather_args, dv.stream())
+    if code == _lib.L1F_ERR_UNSUPPORTED:
+        _lib.call("l1f_gather", *gather_args[:7], _lib.F32, *gather_args[7:], dv.stream())
+        zc, _, itc, rc, stc = filter_units(xc, plan.u, adm, want_e=False, workspace=plan.workspace)
+    else:
+        _lib.check(code, "l1f_filter_with_gather_f32")
     if events is not None:
         events[3].record()
     nr = len(plan.comp_rows)
@@ -352,14 +368,20 @@ def solve_step(plan, mt, l_out=None, s_out=None, events=None):
     if events is not None:
         events[2].record()  # creates the event; re-recorded by the library after the filter launch
         ev_done = events[2].cuda_event
-    beta0 = float(adm.beta0) if adm.beta0 is not None else 0.0
-    beta_max = float(adm.beta_max) if adm.beta_max is not None else 0.0
-    _lib.call("l1f_rowfilter_reconstruct_f32", dv.ptr(xr), xr.stride(0), len(seed.col_idx), nr, dv.ptr(plan.v),
+    code = _lib.load().l1f_rowfilter_reconstruct_f32(dv.ptr(xr), xr.stride(0), len(seed.col_idx), nr, dv.ptr(plan.v),
               plan.v.stride(0), k, float(adm.tol), float(adm.rho), beta0, beta_max, int(adm.max_iter), dv.ptr(zr),
               zr.stride(0), dv.ptr(itr), dv.ptr(rr), dv.ptr(st_r), dv.ptr(plan.d_comp_rows_local),
               dv.ptr(plan.d_row_idx), len(seed.row_idx), dv.ptr(seed.u), dv.ptr(seed.sigma), dv.ptr(plan.d_col_idx),
               len(seed.col_idx), dv.ptr(seed.v), dv.ptr(zc), zc.stride(0), dv.ptr(mt), m, n, mt.stride(0), dv.ptr(l_out), l_out.stride(0), dv.ptr(s_out), s_out.stride(0),
               dv.ptr(rs), ev_done, dv.stream())
+    if code == _lib.L1F_ERR_UNSUPPORTED:  # e.g. an L1F_RECON_STREAM=0 / L1F_RECON_TC=0 override: separate calls
+        zr, _, itr, rr, st_r = filter_units(xr, plan.v, adm, want_e=False, workspace=plan.workspace)
+        if events is not None:
+            events[2].record()
+        af, bf = build_factors(plan, zc, zr)
+        l_out, s_out, rs = reconstruct(mt, af, bf, l_out, s_out)
+    else:
+        _lib.check(code, "l1f_rowfilter_reconstruct_f32")
     if events is not None:
         events[4].record()
     return dict(zc=zc, zr=zr, ec=None, er=None, iters_c=itc, iters_r=itr, res_c=rc, res_r=rr, status_c=stc,
