@@ -3,7 +3,11 @@
 Rank g owns the row block [r0_g, r1_g) of M.  The exchange steps are the ones the algorithm
 has; everything else is local:
 
-  1. all-gather of the seed rows M[row_idx, :]   (each rank contributes the seed rows it owns)
+  1. all-to-all of the column panel: rank h needs M[row_idx, C_h] for its column units C_h, and
+     each rank owns the seed rows inside its row block, so rank g sends M[its seed rows, C_h]
+     to rank h (n_c * s_r floats in total, each rank receiving only its own columns; an
+     all-gather of whole seed rows would move world x more).  The seed solve (t1, once) uses
+     an all-gather of the s_r x s_c seed block's rows.
   2. rank 0 solves the seed PCP on M[row_idx, col_idx]; U, sigma, V are broadcast
   3. column units (all non-seed columns) are split evenly across ranks; row units are the
      non-seed rows of each rank's own block                          (local ADM filters)
@@ -92,6 +96,33 @@ def gather_seed_rows(m_local, plan, group=None):
     return _all_gather_rows(local, counts, group)
 
 
+def exchange_column_panel(m_local, plan, backend, group=None, out=None):
+    """Exchange 1: this rank's column panel Xc[j][p] = M[row_idx[p], my_cols[j]] (unit-major).
+
+    row_idx is sorted and the row blocks are contiguous in rank order, so rank g owns the seed
+    positions [p0_g, p0_g + P_g): it gathers M[its seed rows, all non-seed columns] transposed
+    (one row per column unit, T[j][p - p0_g]); rows [c0_h, c1_h) of T go to rank h
+    (all_to_all_single), and rank h concatenates the received blocks along p in rank order."""
+    world = plan.world
+    local_rows = plan.row_idx[plan.my_seed_pos] - plan.r0
+    if world == 1:
+        return backend.panel_t(m_local, local_rows, plan.comp_cols, out=out)
+    seed_counts = [int((plan.seed_owner == g).sum()) for g in range(world)]
+    col_counts = [c1 - c0 for c0, c1 in plan.col_units]
+    p_me, c_me = seed_counts[plan.rank], col_counts[plan.rank]
+    t = backend.panel_t(m_local, local_rows, plan.comp_cols)        # (n_c, P_me)
+    recv = t.new_empty((c_me * len(plan.row_idx),))
+    dist.all_to_all_single(recv, t.reshape(-1), [c_me * p for p in seed_counts], [c * p_me for c in col_counts],
+                           group=group)
+    blocks, off = [], 0
+    for p in seed_counts:
+        blocks.append(recv[off:off + c_me * p].view(c_me, p))
+        off += c_me * p
+    if out is None:
+        return torch.cat(blocks, dim=1)
+    return torch.cat(blocks, dim=1, out=out)
+
+
 def seed_factors(seed_rows, plan, backend, adm, rank_tol=1e-6, group=None):
     """Exchange 2: rank 0 solves the seed PCP, U / sigma / V are broadcast."""
     dev = seed_rows.device
@@ -117,10 +148,9 @@ def solve_from_seed(m_local, plan, backend, adm, u, sig, v, group=None):
     reconstruction, statistics.  Returns (L_local, S_local, info)."""
     t = {}
     t0 = time.perf_counter()
-    seed_rows = gather_seed_rows(m_local, plan, group)
-    t["seed_rows"] = time.perf_counter() - t0
+    xc = exchange_column_panel(m_local, plan, backend, group)             # (my cols, s_r) unit-major
+    t["column_panel"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    xc = backend.column_panel(seed_rows, plan.my_cols)                    # (my cols, s_r) unit-major
     xr = backend.row_panel(m_local, plan.my_rows - plan.r0, plan.col_idx)  # (my rows, s_c)
     zc, itc, stc = backend.filter(xc, u, adm)
     zr, itr, st_r = backend.filter(xr, v, adm)
@@ -169,6 +199,16 @@ class CudaBackend:
 
     def column_panel(self, seed_rows, cols):
         return self.engine.gather(seed_rows, None, cols, transpose=True)
+
+    def panel_t(self, m_local, local_rows, cols, out=None):
+        """M_local[rows][:, cols] transposed (one row per column), into `out` if given."""
+        if out is None:
+            return self.engine.gather(m_local, local_rows, cols, transpose=True)
+        rt, ct = self.engine.index_tensor(local_rows), self.engine.index_tensor(cols)
+        self.lib.call("l1f_gather", self.dv.dtype_code(m_local), self.dv.ptr(m_local), m_local.stride(0),
+                      self.dv.ptr(rt), len(local_rows), self.dv.ptr(ct), len(cols), self.dv.dtype_code(out),
+                      self.dv.ptr(out), out.stride(0), 1, self.dv.stream())
+        return out
 
     def row_panel(self, m_local, local_rows, cols):
         return self.engine.gather(m_local, local_rows, cols)
@@ -234,6 +274,17 @@ class CudaShardedStep:
         self.l = torch.empty_like(m_local)
         self.s = torch.empty_like(m_local)
         self.xc = torch.empty((len(plan.my_cols), len(plan.row_idx)), dtype=self.fdt, device="cuda")
+        self.d_comp_cols = idx(plan.comp_cols)
+        if plan.world > 1:  # exchange 1 buffers (all-to-all of the column panel)
+            p_me, c_me = self.seed_counts[plan.rank], self.col_counts[plan.rank]
+            self.t_send = torch.empty((len(plan.comp_cols), p_me), dtype=self.fdt, device="cuda")
+            self.recv = torch.empty((c_me * len(plan.row_idx),), dtype=self.fdt, device="cuda")
+            self.out_splits = [c_me * q for q in self.seed_counts]
+            self.in_splits = [c * p_me for c in self.col_counts]
+            self.recv_blocks, off = [], 0
+            for q in self.seed_counts:
+                self.recv_blocks.append(self.recv[off:off + c_me * q].view(c_me, q))
+                off += c_me * q
         self.xr = torch.empty((len(plan.my_rows), len(plan.col_idx)), dtype=self.fdt, device="cuda")
         code = _lib.F32 if self.fdt == torch.float32 else _lib.F64
         nbytes = max(_lib.load().l1f_filter_workspace_bytes(code, len(plan.row_idx), self.k, max(1, len(plan.my_cols))),
@@ -245,13 +296,18 @@ class CudaShardedStep:
     def step(self, m_local, events=None):
         from .l1reg import filter_units
         dv, lib, p = self.dv, self.lib, self.plan
-        local = m_local[self.d_seed_local]
-        seed_rows = _all_gather_rows(local, self.seed_counts, self.group)   # exchange 1
         code_in = dv.dtype_code(m_local)
         code_f = lib.F32 if self.fdt == torch.float32 else lib.F64
-        lib.call("l1f_gather", dv.dtype_code(seed_rows), dv.ptr(seed_rows), seed_rows.stride(0), None,
-                 seed_rows.shape[0], dv.ptr(self.d_my_cols), len(p.my_cols), code_f, dv.ptr(self.xc),
-                 self.xc.stride(0), 1, dv.stream())
+        # exchange 1 (all-to-all): T[j][p] = M[my seed rows, all non-seed columns]; rows of T for
+        # rank h's column units go to h; received blocks concatenate along p into xc
+        tgt = self.xc if p.world == 1 else self.t_send
+        lib.call("l1f_gather", code_in, dv.ptr(m_local), m_local.stride(0), dv.ptr(self.d_seed_local),
+                 self.n_local_seed, dv.ptr(self.d_comp_cols), len(p.comp_cols), code_f, dv.ptr(tgt), tgt.stride(0),
+                 1, dv.stream())
+        if p.world > 1:
+            dist.all_to_all_single(self.recv, self.t_send.reshape(-1), self.out_splits, self.in_splits,
+                                   group=self.group)
+            torch.cat(self.recv_blocks, dim=1, out=self.xc)
         lib.call("l1f_gather", code_in, dv.ptr(m_local), m_local.stride(0), dv.ptr(self.d_my_rows_local),
                  len(p.my_rows), dv.ptr(self.d_col_idx), len(p.col_idx), code_f, dv.ptr(self.xr), self.xr.stride(0), 0,
                  dv.stream())

@@ -36,6 +36,13 @@ class OracleBackend:
     def column_panel(self, seed_rows, cols):
         return seed_rows[:, torch.as_tensor(cols)].t().contiguous()
 
+    def panel_t(self, m_local, local_rows, cols, out=None):
+        t = m_local[torch.as_tensor(local_rows, dtype=torch.int64)][:, torch.as_tensor(cols)].t().contiguous()
+        if out is not None:
+            out.copy_(t)
+            return out
+        return t
+
     def row_panel(self, m_local, local_rows, cols):
         return m_local[torch.as_tensor(local_rows)][:, torch.as_tensor(cols)].contiguous()
 
@@ -124,10 +131,13 @@ def test_shard_plan_partitions_units():
     assert pdist.row_ranges(10, 3) == [(0, 4), (4, 7), (7, 10)]
 
 
-@pytest.mark.timeout(600)
+@pytest.mark.timeout(900)
 def test_sharded_solve_matches_single_process_and_oracle():
     l1, s1, r1 = _run(1)
     l2, s2, r2 = _run(2)
+    l3, s3, r3 = _run(3)  # uneven seed-row and column-unit counts in the all-to-all
+    np.testing.assert_allclose(l3, l1, rtol=0, atol=1e-10 * np.abs(l1).max())
+    np.testing.assert_allclose(s3, s1, rtol=0, atol=1e-10 * np.abs(s1).max())
     assert r2[0][4] == r1[0][4]                 # same seed rank
     assert r2[0][5] == r1[0][5]                 # all units accounted for
     np.testing.assert_allclose(l2, l1, rtol=0, atol=1e-10 * np.abs(l1).max())
@@ -137,3 +147,40 @@ def test_sharded_solve_matches_single_process_and_oracle():
     ref = pipeline.solve(mm, 2, 0, tol=1e-9)
     assert np.linalg.norm(l2 - ref["l"]) <= 1e-8 * np.linalg.norm(ref["l"])
     assert np.linalg.norm(l2 - l0) <= 1e-5 * np.linalg.norm(l0)
+
+
+def _exchange_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        m, n = 50, 37
+        mm = rng.standard_normal((m, n))
+        ri = np.arange(0, 9)                   # every seed row in rank 0's block: others send nothing
+        ci = np.array([0, 5, 11, 20, 36])
+        plan = pdist.ShardPlan(m, n, rank, world, ri, ci)
+        m_local = torch.from_numpy(mm[plan.r0:plan.r1].copy())
+        xc = pdist.exchange_column_panel(m_local, plan, OracleBackend())
+        out_q.put((rank, bool(np.array_equal(xc.numpy(), mm[np.ix_(ri, plan.my_cols)].T))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_column_panel_all_to_all_exchange():
+    """Exchange 1 (all-to-all of M[row_idx, C_h]) equals the direct gather, with ranks that own
+    no seed rows and uneven column-unit counts."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    procs = [ctx.Process(target=_exchange_worker, args=(g, world, port, q)) for g in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)

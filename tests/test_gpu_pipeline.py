@@ -241,6 +241,39 @@ def test_sharded_cuda_backend_matches_single_gpu_solve():
     assert torch.equal(l, sol.l) and torch.equal(s, sol.s)
 
 
+@pytest.mark.parametrize("m,n,r", [(600, 500, 5), (2000, 1800, 30)])
+def test_sharded_timed_step_matches_single_gpu_solve(m, n, r):
+    """The timed multi-GPU step (distributed.CudaShardedStep: column-panel exchange, paired
+    filters, Q~ all-gather, factors, reconstruction) at NCCL world size 1 equals the public
+    single-GPU solve bitwise, for the FP64 small-k and the fp32 tensor-core filter."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_1108_5359_b200 import distributed as pdist
+
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=4)
+    adm = l1pcp.AdmConfig(tol=1e-7)
+    sol = l1pcp.estimate_rank_and_solve(mt, l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=adm))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ri, ci = engine.sample_indices(m, n, 10 * r, 10 * r, np.random.SeedSequence(0).spawn(1)[0])
+        plan = pdist.ShardPlan(m, n, 0, 1, ri, ci)
+        seed_rows = pdist.gather_seed_rows(mt, plan)
+        u, sig, v, _ = pdist.seed_factors(seed_rows, plan, pdist.CudaBackend(), adm)
+        stepper = pdist.CudaShardedStep(mt, plan, adm, u, sig, v)
+        for _ in range(2):
+            l, s, stats, _ = stepper.step(mt)
+            torch.cuda.synchronize()
+            assert torch.equal(l, sol.l) and torch.equal(s, sol.s)
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("m,n,r", [(300, 300, 20), (500, 200, 30), (150, 400, 10)])
 def test_svd_gram_matches_gesvd_on_low_rank(m, n, r):
     """l1f_svd_gram_f64 (the seed's final factorisation) vs l1f_svd_f64 on an exactly rank-r
