@@ -292,6 +292,64 @@ class CudaShardedStep:
         self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
         self._n_units_t = None
         self.launches_per_step = 11  # 2 gathers, 2 scale prologues + 1-2 filter grids, factors, 2 splits, recon, sum
+        # large shards (the library's pass model runs the two unit sets as two launches): the
+        # column filter with the row panel gathered beside it, Q~ all-gather, then the row filter
+        # with the reconstruction of the rank's rows streamed beside it (as engine.solve_step)
+        self.streamed = False
+        if (self.fdt == torch.float32 and dt == torch.float32 and 16 < self.k <= 224 and len(plan.my_cols) > 0
+                and len(plan.my_rows) > 0 and len(plan.row_idx) == len(plan.col_idx)
+                and os.environ.get("L1F_RECON_STREAM") != "0" and m_local.stride(0) % 4 == 0
+                and m_local.data_ptr() % 16 == 0):
+            import ctypes
+            one = ctypes.c_int32(0)
+            _lib.call("l1f_filter_pair_plan_f32", len(plan.row_idx), self.k, len(plan.my_cols), len(plan.my_rows),
+                      ctypes.addressof(one))
+            self.streamed = not one.value
+            force = os.environ.get("L1F_SHARDED_STREAM")  # tests: "1" / "0" overrides the pass model
+            if force in ("0", "1"):
+                self.streamed = force == "1"
+        if self.streamed:
+            nc, nr = len(plan.my_cols), len(plan.my_rows)
+            self.zc = torch.empty((nc, self.k), dtype=torch.float32, device="cuda")
+            self.itc = torch.empty(nc, dtype=torch.int32, device="cuda")
+            self.rc = torch.empty(nc, dtype=torch.float32, device="cuda")
+            self.stc = torch.empty(nc, dtype=torch.uint8, device="cuda")
+            self.zr = torch.empty((nr, self.k), dtype=torch.float32, device="cuda")
+            self.itr = torch.empty(nr, dtype=torch.int32, device="cuda")
+            self.rr = torch.empty(nr, dtype=torch.float32, device="cuda")
+            self.st_r = torch.empty(nr, dtype=torch.uint8, device="cuda")
+            self.rs = torch.zeros(2, dtype=torch.float64, device="cuda")
+            self.launches_per_step = 14  # 2 gathers, 2 x (scale + filter), gate, Bf, strip index, Bf split,
+            #                              concurrent + trailing reconstruction, residual sum
+
+    def _step_streamed(self, m_local, events=None):
+        dv, lib, p, adm = self.dv, self.lib, self.plan, self.adm
+        s_r = len(p.row_idx)
+        beta0 = float(adm.beta0) if adm.beta0 is not None else 0.0
+        beta_max = float(adm.beta_max) if adm.beta_max is not None else 0.0
+        ev_done = None
+        if events is not None:
+            events[0].record()
+            events[1].record()  # creates the event; re-recorded by the library after the row filter
+            ev_done = events[1].cuda_event
+        code = lib.load().l1f_filter_with_gather_f32(
+            dv.ptr(self.xc), self.xc.stride(0), s_r, len(p.my_cols), dv.ptr(self.u), self.u.stride(0), self.k,
+            float(adm.tol), float(adm.rho), beta0, beta_max, int(adm.max_iter), dv.ptr(self.zc), self.zc.stride(0),
+            dv.ptr(self.itc), dv.ptr(self.rc), dv.ptr(self.stc), dv.dtype_code(m_local), dv.ptr(m_local),
+            m_local.stride(0), dv.ptr(self.d_my_rows_local), len(p.my_rows), dv.ptr(self.d_col_idx), len(p.col_idx),
+            dv.ptr(self.xr), self.xr.stride(0), 0, dv.stream())
+        lib.check(code, "l1f_filter_with_gather_f32")
+        zc_all = _all_gather_rows(self.zc, self.col_counts, self.group)          # exchange 2: Q~
+        code = lib.load().l1f_rowfilter_reconstruct_f32(
+            dv.ptr(self.xr), self.xr.stride(0), len(p.col_idx), len(p.my_rows), dv.ptr(self.v), self.v.stride(0),
+            self.k, float(adm.tol), float(adm.rho), beta0, beta_max, int(adm.max_iter), dv.ptr(self.zr),
+            self.zr.stride(0), dv.ptr(self.itr), dv.ptr(self.rr), dv.ptr(self.st_r), dv.ptr(self.d_my_rows_local),
+            dv.ptr(self.d_local_seed_rows), self.n_local_seed, dv.ptr(self.u_local), dv.ptr(self.sig),
+            dv.ptr(self.d_col_idx), len(p.col_idx), dv.ptr(self.v64), dv.ptr(zc_all), zc_all.stride(0),
+            dv.ptr(m_local), p.r1 - p.r0, p.n, m_local.stride(0), dv.ptr(self.l), self.l.stride(0), dv.ptr(self.s),
+            self.s.stride(0), dv.ptr(self.rs), ev_done, dv.stream())
+        lib.check(code, "l1f_rowfilter_reconstruct_f32")
+        return self.zc, self.itc, self.stc, self.zr, self.itr, self.st_r
 
     def step(self, m_local, events=None):
         from .l1reg import filter_units
@@ -308,6 +366,9 @@ class CudaShardedStep:
             dist.all_to_all_single(self.recv, self.t_send.reshape(-1), self.out_splits, self.in_splits,
                                    group=self.group)
             torch.cat(self.recv_blocks, dim=1, out=self.xc)
+        if self.streamed:
+            zc, itc, stc, zr, itr, st_r = self._step_streamed(m_local, events)
+            return self._finish(m_local, itc, stc, itr, st_r)
         lib.call("l1f_gather", code_in, dv.ptr(m_local), m_local.stride(0), dv.ptr(self.d_my_rows_local),
                  len(p.my_rows), dv.ptr(self.d_col_idx), len(p.col_idx), code_f, dv.ptr(self.xr), self.xr.stride(0), 0,
                  dv.stream())
@@ -331,6 +392,9 @@ class CudaShardedStep:
                  dv.ptr(self.v64), dv.ptr(zc_all), zc_all.stride(0), dv.ptr(zr), max(zr.stride(0), self.k),
                  dv.ptr(self.af), dv.ptr(self.bf), dv.stream())
         self.e.reconstruct(m_local, self.af, self.bf, self.l, self.s)
+        return self._finish(m_local, itc, stc, itr, st_r)
+
+    def _finish(self, m_local, itc, stc, itr, st_r):
         dev = m_local.device
         it = torch.stack([itc.max() if itc.numel() else torch.zeros((), dtype=itc.dtype, device=dev),
                           itr.max() if itr.numel() else torch.zeros((), dtype=itr.dtype, device=dev)]).max()

@@ -241,8 +241,9 @@ def test_sharded_cuda_backend_matches_single_gpu_solve():
     assert torch.equal(l, sol.l) and torch.equal(s, sol.s)
 
 
-@pytest.mark.parametrize("m,n,r", [(600, 500, 5), (2000, 1800, 30)])
-def test_sharded_timed_step_matches_single_gpu_solve(m, n, r):
+@pytest.mark.parametrize("m,n,r,stream", [(600, 500, 5, None), (2000, 1800, 30, "0"), (2000, 1800, 30, "1"),
+                                          (3000, 2800, 60, "1")])
+def test_sharded_timed_step_matches_single_gpu_solve(m, n, r, stream, monkeypatch):
     """The timed multi-GPU step (distributed.CudaShardedStep: column-panel exchange, paired
     filters, Q~ all-gather, factors, reconstruction) at NCCL world size 1 equals the public
     single-GPU solve bitwise, for the FP64 small-k and the fp32 tensor-core filter."""
@@ -265,7 +266,11 @@ def test_sharded_timed_step_matches_single_gpu_solve(m, n, r):
         plan = pdist.ShardPlan(m, n, 0, 1, ri, ci)
         seed_rows = pdist.gather_seed_rows(mt, plan)
         u, sig, v, _ = pdist.seed_factors(seed_rows, plan, pdist.CudaBackend(), adm)
+        if stream is not None:  # the paired-filter step, or the streamed one (filter + reconstruction)
+            monkeypatch.setenv("L1F_SHARDED_STREAM", stream)
         stepper = pdist.CudaShardedStep(mt, plan, adm, u, sig, v)
+        if stream is not None:
+            assert stepper.streamed == (stream == "1")
         for _ in range(2):
             l, s, stats, _ = stepper.step(mt)
             torch.cuda.synchronize()
