@@ -66,6 +66,7 @@ class ClockSampler:
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.pre = []
 
     def __enter__(self):
         try:
@@ -82,6 +83,7 @@ class ClockSampler:
             t0 = time.time()
             while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
                 time.sleep(0.005)
+            self.pre = list(self.lines)  # the sample just before the timed region
             self.lines.clear()
         except OSError:
             self.proc = None
@@ -100,6 +102,9 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        window = "timed region"
+        if not self.lines and getattr(self, "pre", None):  # region shorter than the 10 ms sampling period
+            self.lines, window = self.pre, "sample taken just before the timed region (region < sampling period)"
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -115,7 +120,7 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def measured_peaks():
