@@ -103,3 +103,31 @@ def test_streamed_policy_and_public_api():
     assert torch.equal(sol.l, ref["l"])
     assert torch.equal(sol.s, ref["s"])
     assert sol.stats["t2"] > 0 and sol.stats["t_assemble"] >= 0
+
+
+@pytest.mark.parametrize("m,n,r", [
+    (600, 520, 17),     # five strips (the last partial), one column-tile item per strip
+    (1200, 1000, 30),   # s_r = 300 of 1200 rows: strips with more than 32 seed rows (the scan path)
+    (4200, 4000, 130),  # k = 130: one slot group (KP 160), 4-stage reconstruction (KJ2 = 3)
+])
+def test_streamed_shapes(m, n, r):
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=9)
+    plan = _plan(mt, r)
+    ref = _solve(mt, plan, streamed=False)
+    got = _solve(mt, plan, streamed=True)
+    assert torch.equal(got["zr"], ref["zr"])
+    assert torch.equal(got["l"], ref["l"])
+    assert torch.equal(got["s"], ref["s"])
+
+
+def test_streamed_library_refusal_falls_back(monkeypatch):
+    """If the library declines the overlapped calls (here: L1F_RECON_STREAM / L1F_GATHER_OVERLAP
+    switched off underneath a forced streamed plan) solve_step falls back to the separate calls."""
+    m, n, r = 3000, 2800, 40
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=12)
+    plan = _plan(mt, r)
+    ref = _solve(mt, plan, streamed=False)
+    monkeypatch.setenv("L1F_RECON_STREAM", "0")
+    monkeypatch.setenv("L1F_GATHER_OVERLAP", "0")
+    got = _solve(mt, plan, streamed=True)
+    assert torch.equal(got["l"], ref["l"]) and torch.equal(got["s"], ref["s"])
