@@ -368,8 +368,9 @@ def run_ours(args):
                          f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
                          f"{m}x{n}"}
 
-    if streamed:  # gathers, unit scale + column filter, Bf; strip index, Bf split, unit scale + row filter,
-        launches_per_step = 2 + 2 + 1 + 8  # gate, concurrent + trailing reconstruction, residual sum
+    if streamed:  # column gather; unit scale + column filter, gate + row gather beside it; unit scale + row
+        # filter, gate, Bf, strip index, Bf split, concurrent + trailing reconstruction, residual sum
+        launches_per_step = 1 + 4 + 9  # = 14, profiles/r1_launches_cfg3_v5.csv
         phases = {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
                   "column_filter": float(np.mean([e[1].elapsed_time(e[3]) for e in ev_all])),
                   "row_filter": float(np.mean([e[3].elapsed_time(e[2]) for e in ev_all])),
