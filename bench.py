@@ -368,17 +368,23 @@ def run_ours(args):
                          f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
                          f"{m}x{n}"}
 
-    if streamed:  # column gather; unit scale + column filter, gate + row gather beside it; unit scale + row
-        # filter, gate, Bf, strip index, Bf split, concurrent + trailing reconstruction, residual sum
-        launches_per_step = 1 + 4 + 9  # = 14, profiles/r1_launches_cfg3_v5.csv
+    small_k = plan.filter_dtype == torch.float64
+    if streamed:
+        if small_k:  # 2 gathers; unit scale + filter x 2; gate, Bf, strip index, concurrent + trailing
+            launches_per_step = 2 + 4 + 6  # reconstruction, residual sum
+        else:  # column gather; unit scale + column filter, gate + row gather beside it; unit scale + row
+            # filter, gate, Bf, strip index, Bf split, concurrent + trailing reconstruction, residual sum
+            launches_per_step = 1 + 4 + 9  # = 14, profiles/r1_launches_cfg3_v5.csv
         phases = {"gather": float(np.mean([e[0].elapsed_time(e[1]) for e in ev_all])),
                   "column_filter": float(np.mean([e[1].elapsed_time(e[3]) for e in ev_all])),
                   "row_filter": float(np.mean([e[3].elapsed_time(e[2]) for e in ev_all])),
                   "filters": t_filter_only,
                   "reconstruct_exposed": t_tail,
                   "reconstruct_standalone": t_recon,
-                  "note": "the reconstruction of each 128-row strip runs beside the row filter on the SMs its "
-                          "clusters leave free once the strip's row units are done; the rest after it",
+                  "note": ("the reconstruction of each 128-row strip runs beside the row filter (on the same SMs "
+                           "as its blocks) once the strip's row units are done; the rest after it" if small_k else
+                           "the reconstruction of each 128-row strip runs beside the row filter on the SMs its "
+                           "clusters leave free once the strip's row units are done; the rest after it"),
                   "t1_seed_s": t1, "generate_s": t_gen}
     else:
         launches_per_step = 2 + 2 * 2 + 1 + 4  # gathers, (unit scale + filter) x 2, factors, split x 2 + recon + sum

@@ -166,6 +166,21 @@ int l1f_rowfilter_reconstruct_f32(const float* X, int64_t ldx, int32_t s, int64_
                                   float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
                                   void* ev_filter_done, void* stream);
 
+/* The same for k <= 16 with the FP64 small-k filter (configs 1 and 4): X, V, Zr, res in FP64;
+ * Zc is the column filter's z rounded to fp32 (as the pipeline's factor build reads it).  The
+ * reconstruction runs beside the filter's blocks on the same SMs.  L, S bitwise those of
+ * l1f_filter_f64 + l1f_build_factors + l1f_reconstruct (float). */
+int l1f_rowfilter_reconstruct_small(const double* X, int64_t ldx, int32_t s, int64_t n_units,
+                                    const double* V, int64_t ldv, int32_t k, double tol, double rho,
+                                    double beta0, double beta_max, int32_t max_iter,
+                                    double* Zr, int64_t ldz, int32_t* iters, double* res, uint8_t* status,
+                                    const int64_t* unit_rows, const int64_t* row_idx, int64_t s_r,
+                                    const double* U, const double* sigma, const int64_t* col_idx,
+                                    int64_t s_c, const double* V64, const float* Zc, int64_t ldzc,
+                                    const float* M, int64_t m, int64_t n, int64_t ldm,
+                                    float* L, int64_t ldl, float* S, int64_t lds, double* resid_sq,
+                                    void* ev_filter_done, void* stream);
+
 /* ------------------------------------------------------------------------------------
  * A filter launch with an index gather beside it — filter_columns (l1filter.py:116-122) while
  * the row panel m[np.ix_(comp_rows, col_idx)] (l1filter.py:243) is extracted: the filter as

@@ -72,6 +72,10 @@ SIGNATURES = {
                                              _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                                              _vp, _i64,
                                              _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "l1f_rowfilter_reconstruct_small": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f64, _f64, _f64, _f64, _i32,
+                                               _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
+                                               _vp, _i64,
+                                               _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "l1f_filter_with_gather_f32": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _i32,
                                           _vp, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64,
                                           _vp, _i64, _i32, _vp]),

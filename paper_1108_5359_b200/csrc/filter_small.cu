@@ -13,6 +13,7 @@
 //    max|r|; every lane takes the same stop decision (l1reg.py:100-128);
 //  * groups pull units from a global counter; a unit's arithmetic never depends on the group.
 #include "common.cuh"
+#include "filter_pair.cuh"
 
 #include <algorithm>
 
@@ -27,6 +28,11 @@ struct Params {
   int64_t n_units, ldx, ldz, lde;
   int max_iter;
   double tol, rho, beta0, beta_max;
+  // progress notification (l1f_rowfilter_reconstruct_small): + 1 to ncnt[nrows[u] >> 7] once
+  // z_u is in global memory, + 1 to *nres per started block (null: off)
+  const int64_t* nrows = nullptr;
+  unsigned* ncnt = nullptr;
+  unsigned* nres = nullptr;
 };
 
 template <typename T>
@@ -39,6 +45,7 @@ adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, 
                  T* __restrict__ res_out, uint8_t* __restrict__ status) {
   constexpr int AST = KM + 1;  // odd row stride: the lanes of a group read distinct banks
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (P.nres && threadIdx.x == 0) atomicAdd(P.nres, 1u);
   T* As = reinterpret_cast<T*>(smem_raw);  // [s_pad][AST], zero padded
   for (int e = threadIdx.x; e < P.s_pad * AST; e += blockDim.x) {
     const int r = e / AST, t = e - (e / AST) * AST;
@@ -158,6 +165,11 @@ adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, 
       if (res_out) res_out[u] = res;
       if (status) status[u] = code;
     }
+    if (P.ncnt) {  // z_u written by the group: count it for the consumer
+      __threadfence();
+      __syncwarp(gmask);
+      if (gl == 0) atomicAdd(&P.ncnt[P.nrows[u] >> 7], 1u);
+    }
   }
 }
 
@@ -183,6 +195,11 @@ __global__ void unit_scale_kernel(const T* __restrict__ X, Params P, T* __restri
         if (res) res[u] = dead ? T(0) : Limits<T>::inf();
         if (status) status[u] = dead ? L1F_UNIT_ZERO : L1F_UNIT_MAXITER;
       }
+      if (P.ncnt) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(&P.ncnt[P.nrows[u] >> 7], 1u);
+      }
     }
   }
 }
@@ -200,6 +217,9 @@ int launch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
     L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the largest shared-memory carveout: the SMs keep room for a reconstruction CTA beside the
+    // filter's blocks (l1f_rowfilter_reconstruct_small); the filter itself uses ~10 KB per block
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 128, smem) != cudaSuccess ||
         blocks_per_sm < 1)
       blocks_per_sm = 1;
@@ -218,13 +238,23 @@ int launch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
   T* scale = (T*)workspace;
   int* queue = (int*)((unsigned char*)workspace + scale_bytes);
   int rc = L1F_OK;
+  tcf::NotifyHost* nh = tcf::g_notify;
+  tcf::g_notify = nullptr;
+  if (nh) {
+    P.nrows = nh->rows;
+    P.ncnt = nh->cnt;
+    P.nres = nh->resident;
+    nh->cluster = 1;
+  }
   unit_scale_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(n_units, 8), 65535), 256, 0, st>>>(
       X, P, scale, Z, E, iters, res, status);
   if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+  if (rc == L1F_OK && nh && nh->after_prologue && cudaEventRecord(nh->after_prologue, st) != cudaSuccess) rc = L1F_ERR_CUDA;
   if (rc == L1F_OK && max_iter > 0) {
     if (cudaMemsetAsync(queue, 0, sizeof(int), st) != cudaSuccess) rc = L1F_ERR_CUDA;
     const int64_t want_blocks = ceil_div(n_units * L, 128);  // one group per unit at most
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want_blocks, (int64_t)blocks_per_sm * num_sms()));
+    if (nh) nh->ctas = grid;
     kern<<<grid, 128, smem, st>>>(X, A, lda, scale, P, queue, Z, E, iters, res, status);
     if (cudaGetLastError() != cudaSuccess) {
       set_error("filter (small-k): launch failed");

@@ -1251,3 +1251,304 @@ extern "C" int l1f_filter_with_gather_f32(const float* X, int64_t ldx, int32_t s
   cudaFreeAsync(resident, st);
   return rc;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Small k (<= 16; the FP64 small-k filter of configs 1 and 4): the same overlap on the SIMT side.
+// The filter's blocks leave registers and most of the shared memory of every SM free, so a
+// 128-thread reconstruction CTA per SM runs BESIDE them (same SMs), streaming M through a
+// cp.async ring (many rows in flight without registers) and consuming 128-row strips as their
+// row units finish (filter_small.cu counts them).  Per entry L = sum_t fma(Af[i][t], Bf[j][t])
+// in the order of reconstruct_stream_kernel (dense.cu) with the same KM, Af and Bf built as
+// l1f_build_factors does from the fp32-rounded filter outputs: L and S are bitwise those of the
+// separate calls.
+template <typename T>
+int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
+                       double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
+                       int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
+                       bool query, size_t* need);
+
+namespace l1f {
+namespace rtc {
+
+constexpr int SK_THREADS = 128;           // 4 columns per thread: 512-column chunks
+constexpr int SK_COLS = 4 * SK_THREADS;
+constexpr int SK_RB = 4;                  // rows per ring stage
+constexpr int SK_NS = 8;                  // ring stages (SK_NS - 1 in flight)
+
+struct SmallStreamArgs {
+  unsigned* item_ctr;
+  const unsigned* ready;
+  const int* skip;
+  int* err;
+  const int64_t* row_idx;
+  const int* strip_p0;
+  const double* U;        // s_r x k
+  const double* sigma;
+  const double* Zr;       // row-filter z (FP64), unit-major
+  int64_t ldzr;
+  int k, ipr, n_items;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa(dst)), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int KM>
+__global__ void __launch_bounds__(SK_THREADS, 4)  // <= 128 registers: fits beside two filter blocks
+recon_small_stream_kernel(const float* __restrict__ Bf, int64_t ldbf, const float* __restrict__ M, int64_t ldm,
+                          float* __restrict__ L, int64_t ldl, float* __restrict__ S, int64_t lds, int64_t m, int64_t n,
+                          SmallStreamArgs SA, double* __restrict__ part) {
+  constexpr int KMP = (KM + 3) / 4 * 4;
+  __shared__ __align__(16) float as[BM][KMP];             // Af rows of the strip
+  extern __shared__ __align__(16) float4 ring_raw[];       // [SK_NS][SK_RB][SK_THREADS] M stages
+  auto ring = reinterpret_cast<float4(*)[SK_RB][SK_THREADS]>(ring_raw);
+  __shared__ float rsig[16];
+  __shared__ int s_item;
+  __shared__ double red[SK_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid % 32;
+  if (SA.skip && *(volatile const int*)SA.skip) return;
+  if (tid < 16) rsig[tid] = tid < SA.k ? (float)(1.0 / SA.sigma[tid]) : 0.f;  // = l1f_build_factors (float)
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = (int)atomicAdd(SA.item_ctr, 1u);
+    __syncthreads();
+    const int w = s_item;
+    if (w >= SA.n_items) break;
+    const int s = w / SA.ipr, c = w - s * SA.ipr;
+    const int64_t i0 = (int64_t)s * BM, i1 = i0 + BM < m ? i0 + BM : m;
+    const int p0 = SA.strip_p0[s], p1 = SA.strip_p0[s + 1];
+    if (tid == 0) wait_geq(SA.ready + s, (unsigned)((i1 - i0) - (p1 - p0)), SA.err, 256);
+    __syncthreads();
+    {  // Af row i0 + tid (l1f_build_factors: U row or fp32(Zr row) * fp32(1 / sigma))
+      const int64_t i = i0 + tid;
+      float a[KMP];
+#pragma unroll
+      for (int t = 0; t < KMP; ++t) a[t] = 0.f;
+      if (i < i1) {
+        int p = p0;
+        while (p < p1 && __ldg(SA.row_idx + p) < i) ++p;
+        if (p < p1 && SA.row_idx[p] == i) {
+#pragma unroll
+          for (int t = 0; t < KM; ++t) if (t < SA.k) a[t] = (float)SA.U[(int64_t)p * SA.k + t];
+        } else {
+          const double* zr = SA.Zr + (i - p) * SA.ldzr;
+#pragma unroll
+          for (int t = 0; t < KM; ++t) if (t < SA.k) a[t] = (float)__ldcg(zr + t) * rsig[t];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < KMP; t += 4) *reinterpret_cast<float4*>(&as[tid][t]) = make_float4(a[t], a[t + 1], a[t + 2], a[t + 3]);
+    }
+    // my 4 columns of Bf
+    const int64_t c0 = (int64_t)c * SK_COLS + 4 * tid;
+    float b[4][KM];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < KM; ++t) b[q][t] = (c0 + q < n && t < SA.k) ? Bf[(c0 + q) * ldbf + t] : 0.f;
+    const int ncol = c0 < n ? (int)(n - c0 < 4 ? n - c0 : 4) : 0;
+    const int nrows = (int)(i1 - i0), nst = (nrows + SK_RB - 1) / SK_RB;
+    auto issue = [&](int g) {  // stage g: rows i0 + SK_RB g ..
+      if (g < nst) {
+#pragma unroll
+        for (int rr = 0; rr < SK_RB; ++rr) {
+          const int r = SK_RB * g + rr;
+          const bool ok = r < nrows && ncol > 0;
+          cp_async16(&ring[g % SK_NS][rr][tid], M + (i0 + (ok ? r : 0)) * ldm + (ncol > 0 ? c0 : 0), ok ? 4 * ncol : 0);
+        }
+      }
+      cp_async_commit();
+    };
+    __syncthreads();  // as[] complete
+#pragma unroll
+    for (int g = 0; g < SK_NS - 1; ++g) issue(g);
+    double m2 = 0.0;
+    for (int g = 0; g < nst; ++g) {
+      cp_async_wait<SK_NS - 2>();  // stage g landed (this thread's copies)
+      issue(g + SK_NS - 1);        // the slot freed by stage g - 1 (read by this thread only)
+      float acc = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < SK_RB; ++rr) {
+        const int r = SK_RB * g + rr;
+        const float4 mv4 = ring[g % SK_NS][rr][tid];
+        acc = fmaf(mv4.x, mv4.x, fmaf(mv4.y, mv4.y, fmaf(mv4.z, mv4.z, fmaf(mv4.w, mv4.w, acc))));
+        if (r >= nrows || ncol == 0) continue;
+        float a[KMP];
+#pragma unroll
+        for (int t = 0; t < KMP; t += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(&as[r][t]);
+          a[t] = v.x; a[t + 1] = v.y; a[t + 2] = v.z; a[t + 3] = v.w;
+        }
+        float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+#pragma unroll
+        for (int t = 0; t < KM; ++t) {
+          l0 = fmaf(a[t], b[0][t], l0);
+          l1 = fmaf(a[t], b[1][t], l1);
+          l2 = fmaf(a[t], b[2][t], l2);
+          l3 = fmaf(a[t], b[3][t], l3);
+        }
+        const int64_t i = i0 + r;
+        if (ncol == 4) {
+          *reinterpret_cast<float4*>(L + i * ldl + c0) = make_float4(l0, l1, l2, l3);
+          *reinterpret_cast<float4*>(S + i * lds + c0) = make_float4(mv4.x - l0, mv4.y - l1, mv4.z - l2, mv4.w - l3);
+        } else {
+          const float lv[4] = {l0, l1, l2, l3}, mv[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < ncol) {
+              L[i * ldl + c0 + q] = lv[q];
+              S[i * lds + c0 + q] = mv[q] - lv[q];
+            }
+        }
+      }
+      m2 += (double)acc;
+    }
+    cp_async_wait<0>();
+    // per-item sum(M^2) (fixed order: warp sums, then the warps in order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    if (lane == 0) red[tid / 32] = m2;
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0;
+      for (int i = 0; i < SK_THREADS / 32; ++i) a += red[i];
+      part[2 * (int64_t)w] = 0.0;
+      part[2 * (int64_t)w + 1] = a;
+    }
+  }
+}
+
+}  // namespace rtc
+}  // namespace l1f
+
+extern "C" int l1f_rowfilter_reconstruct_small(
+    const double* Xr, int64_t ldx, int32_t s, int64_t n_units, const double* V, int64_t ldv, int32_t k, double tol,
+    double rho, double beta0, double beta_max, int32_t max_iter, double* Zr, int64_t ldz, int32_t* iters, double* res,
+    uint8_t* status, const int64_t* unit_rows, const int64_t* row_idx, int64_t s_r, const double* U,
+    const double* sigma, const int64_t* col_idx, int64_t s_c, const double* V64, const float* Zc, int64_t ldzc,
+    const float* M, int64_t m, int64_t n, int64_t ldm, float* L, int64_t ldl, float* S, int64_t lds,
+    double* resid_sq, void* ev_filter_done, void* stream) {
+  using namespace l1f;
+  using namespace l1f::rtc;
+  L1F_REQUIRE(m >= 1 && n >= 1 && k >= 1 && s >= 1 && s_r >= 0 && s_r <= m && n_units == m - s_r, L1F_ERR_ARG,
+              "rowfilter_reconstruct_small: need the m - s_r non-seed rows as units");
+  L1F_REQUIRE(ldx >= s && ldz >= k && ldv >= k && ldzc >= k && ldm >= n && ldl >= n && lds >= n && s_c >= 0 && s_c <= n,
+              L1F_ERR_ARG, "rowfilter_reconstruct_small: leading dimension too small");
+  L1F_REQUIRE(M && L && S && Zr && (s_r == 0 || (U && row_idx)) && (s_c == 0 || (V64 && col_idx)) && sigma &&
+                  (s_c == n || Zc),
+              L1F_ERR_ARG, "rowfilter_reconstruct_small: null operand");
+  const char* env = getenv("L1F_RECON_STREAM");
+  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  if (k > 16 || !al16(M) || !al16(L) || !al16(S) || ldm % 4 || ldl % 4 || lds % 4 || m >= INT32_MAX / 2 ||
+      n >= INT32_MAX / 2)
+    return L1F_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  SideStream* side = side_stream();
+  if (!side) return L1F_ERR_UNSUPPORTED;
+  const int km = 2 * ((k + 1) / 2);  // reconstruct_stream_kernel's KM for float
+  const int ntm = (int)ceil_div(m, BM);
+  const int ipr = (int)ceil_div(n, SK_COLS);
+  const int64_t n_items64 = (int64_t)ntm * ipr;
+  L1F_REQUIRE(n_items64 < INT32_MAX / 2, L1F_ERR_UNSUPPORTED, "rowfilter_reconstruct_small: too many items");
+  const int n_items = (int)n_items64;
+  float* bf = nullptr;
+  double* part = nullptr;
+  unsigned* ctr = nullptr;
+  L1F_CUDA_TRY(cudaMallocAsync(&bf, sizeof(float) * (size_t)n * k, st));
+  L1F_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * 2 * (size_t)n_items, st));
+  // counters: item_ctr, resident, skip, err | ready[ntm] | strip_p0[ntm + 1]
+  const size_t n_ctr = 4 + 2 * (size_t)ntm + 1;
+  L1F_CUDA_TRY(cudaMallocAsync(&ctr, sizeof(unsigned) * n_ctr, st));
+  unsigned* item_ctr = ctr;
+  unsigned* resident = ctr + 1;
+  int* skip = reinterpret_cast<int*>(ctr + 2);
+  int* err = reinterpret_cast<int*>(ctr + 3);
+  unsigned* ready = ctr + 4;
+  int* strip_p0 = reinterpret_cast<int*>(ready + ntm);
+  const int nsm = num_sms();
+  int rc = cudaMemsetAsync(ctr, 0, sizeof(unsigned) * n_ctr, st) == cudaSuccess ? L1F_OK : L1F_ERR_CUDA;
+  auto prologue = [&](cudaStream_t q) -> int {
+    int r = l1f_build_factors(L1F_F32, 0, n, k, nullptr, 0, col_idx, s_c, nullptr, sigma, V64, Zc, ldzc, nullptr, k,
+                              nullptr, bf, q);
+    if (r != L1F_OK) return r;
+    strip_p0_kernel<<<(unsigned)ceil_div(ntm + 1, 256), 256, 0, q>>>(row_idx, s_r, ntm, strip_p0);
+    return cudaGetLastError() == cudaSuccess ? L1F_OK : L1F_ERR_CUDA;
+  };
+  tcf::NotifyHost nh;
+  if (rc == L1F_OK) {
+    nh.rows = unit_rows;
+    nh.cnt = ready;
+    nh.resident = resident;
+    nh.after_prologue = side->e0;
+    tcf::g_notify = &nh;
+    rc = l1f_small_dispatch<double>(Xr, ldx, s, n_units, V, ldv, k, tol, rho, beta0, beta_max, max_iter, Zr, ldz, nullptr,
+                                    s, iters, res, status, nullptr, 0, st, false, nullptr);
+    tcf::g_notify = nullptr;
+    if (rc == L1F_OK && nh.cluster == 0) rc = L1F_ERR_UNSUPPORTED;  // the small-k filter did not run
+  }
+  if (rc == L1F_OK && ev_filter_done && cudaEventRecord((cudaEvent_t)ev_filter_done, st) != cudaSuccess) rc = L1F_ERR_CUDA;
+  if (rc == L1F_OK) {
+    SmallStreamArgs SA;
+    SA.item_ctr = item_ctr; SA.ready = ready; SA.skip = nullptr; SA.err = err; SA.row_idx = row_idx;
+    SA.strip_p0 = strip_p0; SA.U = U; SA.sigma = sigma; SA.Zr = Zr; SA.ldzr = ldz; SA.k = k; SA.ipr = ipr;
+    SA.n_items = n_items;
+    auto launch = [&](int grid, cudaStream_t q, const int* skip_) -> bool {
+      SmallStreamArgs a = SA;
+      a.skip = skip_;
+      constexpr size_t ring_bytes = sizeof(float4) * SK_NS * SK_RB * SK_THREADS;
+#define L1F_SKS(KMV)                                                                                          \
+  {                                                                                                           \
+    static std::once_flag once;                                                                               \
+    std::call_once(once, [] {                                                                                 \
+      cudaFuncSetAttribute(recon_small_stream_kernel<KMV>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                           (int)ring_bytes);                                                                  \
+    });                                                                                                       \
+    recon_small_stream_kernel<KMV><<<grid, SK_THREADS, ring_bytes, q>>>(bf, k, M, ldm, L, ldl, S, lds, m, n, a, part); \
+  }
+      switch (km) {
+        case 2: L1F_SKS(2); break;
+        case 4: L1F_SKS(4); break;
+        case 6: L1F_SKS(6); break;
+        case 8: L1F_SKS(8); break;
+        case 10: L1F_SKS(10); break;
+        case 12: L1F_SKS(12); break;
+        case 14: L1F_SKS(14); break;
+        default: L1F_SKS(16); break;
+      }
+#undef L1F_SKS
+      return cudaGetLastError() == cudaSuccess;
+    };
+    const char* ce = getenv("L1F_RECON_CONCURRENT");
+    const bool concurrent = nh.ctas > 0 && !(ce && ce[0] == '0');
+    if (concurrent) {  // one CTA per SM beside the filter's blocks, once they are all resident
+      if (cudaStreamWaitEvent(side->st, side->e0, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+      if (rc == L1F_OK) {
+        recon_gate_kernel<<<1, 32, 0, side->st>>>(resident, (unsigned)nh.ctas, skip, 1000ull * 1000);
+        if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+      }
+      if (rc == L1F_OK) rc = prologue(side->st);
+      if (rc == L1F_OK && (cudaEventRecord(side->e2, side->st) != cudaSuccess ||
+                           !launch(std::min(nsm, n_items), side->st, skip) ||
+                           cudaEventRecord(side->e1, side->st) != cudaSuccess))
+        rc = L1F_ERR_CUDA;
+      if (rc == L1F_OK && cudaStreamWaitEvent(st, side->e2, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+    } else if (rc == L1F_OK) {
+      rc = prologue(st);
+    }
+    if (rc == L1F_OK && !launch((int)std::min<int64_t>((int64_t)nsm * 8, n_items), st, nullptr)) rc = L1F_ERR_CUDA;
+    if (concurrent && cudaStreamWaitEvent(st, side->e1, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
+    if (rc == L1F_OK && resid_sq) {
+      sum_items_kernel<<<1, 1024, 0, st>>>(part, n_items, err, resid_sq);
+      if (cudaGetLastError() != cudaSuccess) rc = L1F_ERR_CUDA;
+    }
+    if (rc == L1F_ERR_CUDA) set_error("rowfilter_reconstruct_small: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFreeAsync(bf, st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(ctr, st);
+  return rc;
+}

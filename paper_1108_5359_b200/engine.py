@@ -307,12 +307,87 @@ def _streamed_ok(plan, mt):
     return not getattr(plan, key)
 
 
+STREAM_SMALL_MIN_ENTRIES = 1 << 24  # below this the small-k reconstruction is too short to overlap
+
+
+def _streamed_small_ok(plan, mt):
+    """The small-k form: FP64 filter (k <= 16) on an fp32 matrix large enough that its
+    reconstruction is worth running beside the row filter (l1f_rowfilter_reconstruct_small)."""
+    if os.environ.get("L1F_RECON_STREAM") == "0" or plan.want_e:
+        return False
+    if not (mt.dtype == torch.float32 and plan.filter_dtype == torch.float64 and plan.k <= 16):
+        return False
+    if plan.row_range != (0, plan.m_rows) or len(plan.comp_cols) != len(plan.comp_cols_all):
+        return False
+    if len(plan.comp_rows) == 0 or plan.m_rows * plan.m_cols < STREAM_SMALL_MIN_ENTRIES:
+        return False
+    return mt.stride(1) == 1 and mt.stride(0) % 4 == 0 and mt.data_ptr() % 16 == 0
+
+
+def _solve_step_small(plan, mt, l_out, s_out, events):
+    """solve_step for the small-k FP64 filter with the reconstruction beside the row filter."""
+    from .l1reg import filter_units
+    seed, adm = plan.seed, plan.adm
+    m, n = mt.shape
+    k = plan.k
+    f64 = torch.float64
+    if events is not None:
+        events[0].record()
+    xc = torch.empty((len(plan.comp_cols), len(seed.row_idx)), dtype=f64, device="cuda")
+    _lib.call("l1f_gather", _lib.F32, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_row_idx), len(seed.row_idx),
+              dv.ptr(plan.d_comp_cols), len(plan.comp_cols), _lib.F64, dv.ptr(xc), xc.stride(0), 1, dv.stream())
+    xr = torch.empty((len(plan.comp_rows), len(seed.col_idx)), dtype=f64, device="cuda")
+    _lib.call("l1f_gather", _lib.F32, dv.ptr(mt), mt.stride(0), dv.ptr(plan.d_comp_rows_local), len(plan.comp_rows),
+              dv.ptr(plan.d_col_idx), len(seed.col_idx), _lib.F64, dv.ptr(xr), xr.stride(0), 0, dv.stream())
+    if events is not None:
+        events[1].record()
+    zc, _, itc, rc, stc = filter_units(xc, plan.u, adm, want_e=False, workspace=plan.workspace)
+    zc32 = zc.to(torch.float32)
+    if events is not None:
+        events[3].record()
+    nr = len(plan.comp_rows)
+    zr = torch.empty((nr, k), dtype=f64, device="cuda")
+    itr = torch.empty(nr, dtype=torch.int32, device="cuda")
+    rr = torch.empty(nr, dtype=f64, device="cuda")
+    st_r = torch.empty(nr, dtype=torch.uint8, device="cuda")
+    l_out = l_out if l_out is not None else torch.empty((m, n), dtype=mt.dtype, device="cuda")
+    s_out = s_out if s_out is not None else torch.empty((m, n), dtype=mt.dtype, device="cuda")
+    rs = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ev_done = None
+    if events is not None:
+        events[2].record()
+        ev_done = events[2].cuda_event
+    beta0 = float(adm.beta0) if adm.beta0 is not None else 0.0
+    beta_max = float(adm.beta_max) if adm.beta_max is not None else 0.0
+    code = _lib.load().l1f_rowfilter_reconstruct_small(
+        dv.ptr(xr), xr.stride(0), len(seed.col_idx), nr, dv.ptr(plan.v), plan.v.stride(0), k, float(adm.tol),
+        float(adm.rho), beta0, beta_max, int(adm.max_iter), dv.ptr(zr), zr.stride(0), dv.ptr(itr), dv.ptr(rr),
+        dv.ptr(st_r), dv.ptr(plan.d_comp_rows_local), dv.ptr(plan.d_row_idx), len(seed.row_idx), dv.ptr(seed.u),
+        dv.ptr(seed.sigma), dv.ptr(plan.d_col_idx), len(seed.col_idx), dv.ptr(seed.v), dv.ptr(zc32),
+        zc32.stride(0), dv.ptr(mt), m, n, mt.stride(0), dv.ptr(l_out), l_out.stride(0), dv.ptr(s_out),
+        s_out.stride(0), dv.ptr(rs), ev_done, dv.stream())
+    if code == _lib.L1F_ERR_UNSUPPORTED:
+        zr, _, itr, rr, st_r = filter_units(xr, plan.v, adm, want_e=False, workspace=plan.workspace)
+        if events is not None:
+            events[2].record()
+        af, bf = build_factors(plan, zc32, zr.to(torch.float32))
+        l_out, s_out, rs = reconstruct(mt, af, bf, l_out, s_out)
+    else:
+        _lib.check(code, "l1f_rowfilter_reconstruct_small")
+    if events is not None:
+        events[4].record()
+    return dict(zc=zc32, zr=zr.to(torch.float32), ec=None, er=None, iters_c=itc, iters_r=itr, res_c=rc, res_r=rr,
+                status_c=stc, status_r=st_r, l=l_out, s=s_out, resid_sq=rs, af=None, bf=None, streamed=True)
+
+
 def solve_step(plan, mt, l_out=None, s_out=None, events=None):
     """One solve from resident seed factors: panels -> column filter -> row filter with Bf and
     the reconstruction streamed beside it (fp32 tensor-core path), else panels -> filters ->
     factors -> reconstruction.  events: optional [start, after_gathers, after_filters,
     before_reconstruct, end] recorded on the current stream (with streaming, after_filters is
     the end of the row-filter launch and the reconstruction overlaps it)."""
+    if _streamed_small_ok(plan, mt):
+        return _solve_step_small(plan, mt, l_out, s_out, events)
     if not _streamed_ok(plan, mt):
         f = filter_stage(plan, mt, events[:3] if events is not None else None)
         af, bf = build_factors(plan, f["zc"], f["zr"])

@@ -131,3 +131,48 @@ def test_streamed_library_refusal_falls_back(monkeypatch):
     monkeypatch.setenv("L1F_GATHER_OVERLAP", "0")
     got = _solve(mt, plan, streamed=True)
     assert torch.equal(got["l"], ref["l"]) and torch.equal(got["s"], ref["s"])
+
+
+def _solve_small(mt, plan, streamed, concurrent=True):
+    old = engine._streamed_small_ok
+    env = os.environ.get("L1F_RECON_CONCURRENT")
+    try:
+        engine._streamed_small_ok = (lambda p, t: True) if streamed else (lambda p, t: False)
+        if not concurrent:
+            os.environ["L1F_RECON_CONCURRENT"] = "0"
+        f = engine.solve_step(plan, mt)
+        torch.cuda.synchronize()
+    finally:
+        engine._streamed_small_ok = old
+        if env is None:
+            os.environ.pop("L1F_RECON_CONCURRENT", None)
+        else:
+            os.environ["L1F_RECON_CONCURRENT"] = env
+    return f
+
+
+@pytest.mark.parametrize("m,n,r,concurrent,kind", [
+    (6000, 3000, 10, True, 0),
+    (6000, 3000, 10, False, 0),
+    (4100, 2050, 3, True, 0),     # ragged strips and 512-column chunks, KM = 4
+    (5000, 2600, 16, True, 0),
+    (7680, 1000, 10, True, 1),    # video kind (moving boxes), the cfg4 statistics
+])
+def test_streamed_small_k_matches_separate_calls(m, n, r, concurrent, kind):
+    """k <= 16: the FP64 small-k filter with the SIMT reconstruction beside it
+    (l1f_rowfilter_reconstruct_small) equals the separate calls bitwise."""
+    from paper_1108_5359_b200 import _lib
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 255.0 if kind else 500.0, seed=13,
+                                         kind=_lib.GEN_VIDEO if kind else _lib.GEN_GAUSSIAN)
+    plan = _plan(mt, r)
+    assert plan.filter_dtype == torch.float64
+    ref = _solve_small(mt, plan, streamed=False)
+    for _ in range(2):
+        got = _solve_small(mt, plan, streamed=True, concurrent=concurrent)
+        assert got.get("streamed")
+        assert torch.equal(got["zr"], ref["zr"])
+        assert torch.equal(got["iters_r"], ref["iters_r"])
+        assert torch.equal(got["l"], ref["l"])
+        assert torch.equal(got["s"], ref["s"])
+        r_ref = ref["resid_sq"].cpu().numpy()  # sum(M^2): fp32 partials grouped differently
+        np.testing.assert_allclose(got["resid_sq"].cpu().numpy(), r_ref, rtol=1e-6, atol=1e-6 * r_ref[1])

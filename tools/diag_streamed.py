@@ -19,15 +19,16 @@ fcfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=1e-7)
 kind, seed, _, _ = engine.seed_stage(mt, fcfg)
 plan = engine.FilterPlan(m, n, seed, mt.dtype, fcfg.adm, want_e=False)
 l_out, s_out = torch.empty_like(mt), torch.empty_like(mt)
-print("streamed_ok", engine._streamed_ok(plan, mt))
+print("streamed_ok", engine._streamed_ok(plan, mt), "small", engine._streamed_small_ok(plan, mt))
 
 
 def run(label, env, force, reps=5):
     old = dict(os.environ)
     os.environ.update(env)
-    ok = engine._streamed_ok
+    ok, oks = engine._streamed_ok, engine._streamed_small_ok
     if force is not None:
-        engine._streamed_ok = lambda p, t: force
+        engine._streamed_ok = lambda p, t: force and p.filter_dtype == torch.float32
+        engine._streamed_small_ok = lambda p, t: force and p.filter_dtype == torch.float64
     try:
         for _ in range(2):
             engine.solve_step(plan, mt, l_out, s_out)
@@ -50,7 +51,7 @@ def run(label, env, force, reps=5):
             engine.solve_step(plan, mt, l_out, s_out)
             torch.cuda.synchronize()
     finally:
-        engine._streamed_ok = ok
+        engine._streamed_ok, engine._streamed_small_ok = ok, oks
         os.environ.clear()
         os.environ.update(old)
 
