@@ -226,6 +226,18 @@ __device__ __forceinline__ void split8(const float (&v)[8], uint4& w0, uint4& w1
   w1 = make_uint4(b[0], b[1], b[2], b[3]);
   w2 = make_uint4(c[0], c[1], c[2], c[3]);
 }
+// the first two pieces only (the residual-form phase c reads v0 and v1)
+__device__ __forceinline__ void split8_store2(const float (&v)[8], __nv_bfloat16* d0, __nv_bfloat16* d1) {
+  uint32_t a[4], b[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float x0 = v[2 * i], x1 = v[2 * i + 1];
+    a[i] = cvt_bf16x2(x0, x1);
+    b[i] = cvt_bf16x2(x0 - bf_lo(a[i]), x1 - bf_hi(a[i]));
+  }
+  *reinterpret_cast<uint4*>(d0) = make_uint4(a[0], a[1], a[2], a[3]);
+  *reinterpret_cast<uint4*>(d1) = make_uint4(b[0], b[1], b[2], b[3]);
+}
 __device__ __forceinline__ void split8_store(const float (&v)[8], __nv_bfloat16* d0, __nv_bfloat16* d1,
                                              __nv_bfloat16* d2) {
   uint4 w0, w1, w2;
@@ -284,6 +296,10 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   // phase c reuses the phase-a columns (az is read out before phase c is issued): 96 per M tile
   // (TA: 64 per M tile)
   constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * MTC;
+  // residual-form z step, z_{it+1} = z_it + A^T (v - A z_it): phase c needs only a 2-piece v and
+  // the a0 v0 + a0 v1 + a1 v0 products (its fixed point does not depend on phase c's precision);
+  // (every variant)
+  constexpr bool RF = true;
   static_assert(!TA || NG == 1, "TA runs one slot group");
   static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
   // NG = 3: the slots' x live in TMEM (32 columns per group, lane = row), not in registers
@@ -584,7 +600,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
         const float tn = pr.y;
         const float x = xr[j];
-        const float azv = (TA && pr.z != 0.f) ? 0.f : az[j];  // non-TA: z = 0 for fresh/empty slots
+        const float azv = (RF && pr.z != 0.f) ? 0.f : az[j];  // non-RF: z = 0 for fresh/empty slots
         const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
         rmax[j] = fabsf(r);
         const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -593,7 +609,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const bool sup = fabsf(w) > tn;
         const float sgt = w > 0.f ? tn : -tn;
         lr[j] = sup ? (azv - yb) + sgt : x;
-        if constexpr (TA) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
+        if constexpr (RF) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
         else az[j] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
         yr[j] = y;
       }
@@ -604,7 +620,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
         const size_t off = (size_t)((lrow >> 3) * 12 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
-        split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+        if constexpr (RF) split8_store2(v8, vop + off, vop + 4 * 64 + off);
+        else split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
       }
       {  // per-slot max|r| over this warp's 32 rows
         const float m = slot_max<SPT>(rmax, lane);
@@ -655,7 +672,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
           const float tn = pr.y;
           const float x = xb[i];
-          const float azv = (TA && pr.z != 0.f) ? 0.f : az[i];  // non-TA: z = 0 for fresh/empty slots
+          const float azv = (RF && pr.z != 0.f) ? 0.f : az[i];  // non-RF: z = 0 for fresh/empty slots
           const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
           rmax[i] = fabsf(r);
           const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -664,7 +681,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const bool sup = fabsf(w) > tn;
           const float sgt = w > 0.f ? tn : -tn;
           lr[j] = sup ? (azv - yb) + sgt : x;
-          if constexpr (TA) az[i] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
+          if constexpr (RF) az[i] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
           else az[i] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
           yr[j] = y;
         }
@@ -675,7 +692,8 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
           for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
           const size_t off = (size_t)((lrow >> 3) * 12 + sb / 8 + hh) * 64 + (lrow & 7) * 8;
-          split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+          if constexpr (RF) split8_store2(v8, vop + off, vop + 4 * 64 + off);
+        else split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
         }
         {  // per-slot max|r| over this warp's 32 rows
           const float m = slot_max<BS>(rmax, lane);
@@ -692,7 +710,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll
-      for (int mt = 0; mt < MTC && TA; ++mt) {  // 3 products of 2-piece A and v': a0 [v0 v1] -> 0-63, a1 [v0] -> 32-63
+      for (int mt = 0; mt < MTC && RF; ++mt) {  // 3 products of 2-piece A and v': a0 [v0 v1] -> 0-63, a1 [v0] -> 32-63
         const uint32_t dc = tmem + 64u * mt;
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
@@ -703,7 +721,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         }
       }
 #pragma unroll
-      for (int mt = 0; mt < MTC && !TA; ++mt) {
+      for (int mt = 0; mt < MTC && !RF; ++mt) {
         const uint32_t dc = tmem + 96u * mt;
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
@@ -816,7 +834,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
       for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
         float zp[SPT];
-        if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+        if constexpr (RF) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
           float b0[SPT], b1[SPT];
           const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)slot0;
           if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
@@ -867,7 +885,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         for (int bk = 0; bk < SPT / BR; ++bk) {
           const int sb = slot0 + BR * bk;
           float zp[BR];
-          if constexpr (TA) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+          if constexpr (RF) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
             float b0[BR], b1[BR];
             const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)sb;
             if constexpr (BR == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
@@ -927,7 +945,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         prof[10] += tdec3 - tdec0;
         prof[14] += __popc(fmask);
       }
-      if constexpr (TA) {
+      if constexpr (RF) {
         const unsigned zm = __ballot_sync(0xffffffffu, !(G.state[lane] == 1) || G.it[lane] == 0);
         if (lane == 0) G.zmask[par ^ 1] = zm;
       }
@@ -944,7 +962,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         // swizzled inbox/slice accesses and the z-operand stores are bank-conflict free
         const int sg = item / vmine, row = item - sg * vmine, t = r0 + row;
         float v8[8];
-        if constexpr (TA) {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
+        if constexpr (RF) {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
           const uint32_t zm = G.zmask[par] >> (8 * sg);
           const float* zrow = zs_prev + (size_t)row * TS;
           const float4 p0 = *reinterpret_cast<const float4*>(zrow + 4 * ((2 * sg) ^ (row & 7)));
@@ -983,7 +1001,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           }
         }
         stamp(7);
-        if constexpr (!TA) {  // slots finished at this pass restart (refill) or idle with z = 0
+        if constexpr (!RF) {  // slots finished at this pass restart (refill) or idle with z = 0
           const uint32_t zf = G.zfin >> (8 * sg);
           if (zf & 0xFFu) {
 #pragma unroll
