@@ -7,8 +7,12 @@
 // k <= 112: 3 x 4 warps; NG = 2 with L1F_TC_NG=2 or when three do not fit: 2 x 8 warps; NG = 1
 // for larger k: 16 warps); a group's pass is one ADM iteration of its 32 units:
 //   phase a   az[row][slot] = sum_t A[row][t] z[t][slot]      tcgen05.mma M=128 (rows) N=32 K=k
-//   phase b   the elementwise ADM update of filter_resident.cu (cancellation-free residual)
-//   phase c   zp[t][slot]   = sum_row A[row][t] v[row][slot]   tcgen05.mma M=128 (t)    N=32 K=128
+//   phase b   the elementwise ADM update of filter_resident.cu (cancellation-free residual),
+//             emitting v' = v - A z_it
+//   phase c   zp[t][slot]   = sum_row A[row][t] v'[row][slot]  tcgen05.mma M=128 (t)    N=32 K=128
+//             (residual form: z_{it+1} = z_it + A^T v', identical to the reference's z = A^T v for
+//             orthonormal A; its fixed point does not depend on phase c's precision, so v' and the
+//             dictionary enter phase c with two bf16 pieces: a0 [v0 v1] + a1 v0, 2 MMAs per K step)
 //   exchange  round 1: each thread pushes its TMEM rows of zp straight to the CTA owning them
 //             (DSMEM st.async) with the per-slot max|r|; the per-unit decision follows; round 2:
 //             owners sum their slice, split it into the bf16 pieces of the phase-a operand and
@@ -106,8 +110,7 @@ struct Group {
   long long head, tail, pf_from, pf_to;
   alignas(8) unsigned long long bar_p, bar_q, bar_r, bar_a, bar_c;
   uint32_t fmask;
-  uint32_t zfin;      // slots finished at this pass (decision part 1): their z goes to 0 in round 2
-  uint32_t zmask[2];  // TA: by pass parity, slots whose z_it is 0 (fresh or empty)
+  uint32_t zmask[2];  // by pass parity, slots whose z_it is 0 (fresh or empty)
 };
 
 template <int KP, int NA>
@@ -296,10 +299,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   // phase c reuses the phase-a columns (az is read out before phase c is issued): 96 per M tile
   // (TA: 64 per M tile)
   constexpr uint32_t GCOLS = TA ? (64u * MTC > 96u ? 64u * MTC : 96u) : 96u * MTC;
-  // residual-form z step, z_{it+1} = z_it + A^T (v - A z_it): phase c needs only a 2-piece v and
-  // the a0 v0 + a0 v1 + a1 v0 products (its fixed point does not depend on phase c's precision);
-  // (every variant)
-  constexpr bool RF = true;
   static_assert(!TA || NG == 1, "TA runs one slot group");
   static_assert(!TA || NA == 2, "TA keeps 2 dictionary pieces in shared memory");
   // NG = 3: the slots' x live in TMEM (32 columns per group, lane = row), not in registers
@@ -600,7 +599,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
         const float tn = pr.y;
         const float x = xr[j];
-        const float azv = (RF && pr.z != 0.f) ? 0.f : az[j];  // non-RF: z = 0 for fresh/empty slots
+        const float azv = pr.z != 0.f ? 0.f : az[j];  // z_it of a fresh or empty slot is 0
         const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
         rmax[j] = fabsf(r);
         const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -609,8 +608,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         const bool sup = fabsf(w) > tn;
         const float sgt = w > 0.f ? tn : -tn;
         lr[j] = sup ? (azv - yb) + sgt : x;
-        if constexpr (RF) az[j] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
-        else az[j] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
+        az[j] = sup ? sgt : (x + yb) - azv;  // v' = v - A z_it (residual-form z step)
         yr[j] = y;
       }
       // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
@@ -620,8 +618,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
         const size_t off = (size_t)((lrow >> 3) * 12 + slot0 / 8 + hh) * 64 + (lrow & 7) * 8;
-        if constexpr (RF) split8_store2(v8, vop + off, vop + 4 * 64 + off);
-        else split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+        split8_store2(v8, vop + off, vop + 4 * 64 + off);
       }
       {  // per-slot max|r| over this warp's 32 rows
         const float m = slot_max<SPT>(rmax, lane);
@@ -672,7 +669,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const float4 pr = G.prm[slot0 + j];  // beta_it, 1/beta_{it+1}, zero-az flag
           const float tn = pr.y;
           const float x = xb[i];
-          const float azv = (RF && pr.z != 0.f) ? 0.f : az[i];  // non-RF: z = 0 for fresh/empty slots
+          const float azv = pr.z != 0.f ? 0.f : az[i];  // z_it of a fresh or empty slot is 0
           const float r = lr[j] - azv;          // r_it = x - A z_it - e_it (0 for fresh and empty slots)
           rmax[i] = fabsf(r);
           const float y = fmaf(pr.x, r, yr[j]);  // y_{it+1} = y_it + b_it r_it
@@ -681,8 +678,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const bool sup = fabsf(w) > tn;
           const float sgt = w > 0.f ? tn : -tn;
           lr[j] = sup ? (azv - yb) + sgt : x;
-          if constexpr (RF) az[i] = sup ? sgt : (x + yb) - azv;  // v - A z_it (residual-form z step)
-          else az[i] = sup ? azv + sgt : x + yb;                // v = (x - e) + y / b
+          az[i] = sup ? sgt : (x + yb) - azv;  // v' = v - A z_it (residual-form z step)
           yr[j] = y;
         }
         // v operand: MN-major core matrices (row group rg, n group 4 p + sg) at (rg * 12 + 4 p + sg) * 64
@@ -692,8 +688,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
           for (int i = 0; i < 8; ++i) v8[i] = az[8 * hh + i];
           const size_t off = (size_t)((lrow >> 3) * 12 + sb / 8 + hh) * 64 + (lrow & 7) * 8;
-          if constexpr (RF) split8_store2(v8, vop + off, vop + 4 * 64 + off);
-        else split8_store(v8, vop + off, vop + 4 * 64 + off, vop + 8 * 64 + off);
+          split8_store2(v8, vop + off, vop + 4 * 64 + off);
         }
         {  // per-slot max|r| over this warp's 32 rows
           const float m = slot_max<BS>(rmax, lane);
@@ -706,11 +701,11 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
     bar_sync(gbar, GT);
     stamp(2);
 
-    // ========== phase c on the tensor core: zp = A_rows^T v
+    // ========== phase c on the tensor core: zp = A_rows^T v' (v' = v - A z_it, residual form)
     if (gw == 1 && lane == 0) {
       umma::fence_after();
 #pragma unroll
-      for (int mt = 0; mt < MTC && RF; ++mt) {  // 3 products of 2-piece A and v': a0 [v0 v1] -> 0-63, a1 [v0] -> 32-63
+      for (int mt = 0; mt < MTC; ++mt) {  // 3 products of 2-piece A and v': a0 [v0 v1] -> 0-63, a1 [v0] -> 32-63
         const uint32_t dc = tmem + 64u * mt;
 #pragma unroll 1
         for (int ks = 0; ks < SL / 16; ++ks) {
@@ -718,19 +713,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const uint64_t db = umma::desc_noswz(v_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
           mma_bf16(dc, umma::desc_noswz(aa, KG * 128, 128), db, ID_C64, ks != 0);
           mma_bf16(dc + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), db, ID_C32, 1u);
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < MTC && !RF; ++mt) {
-        const uint32_t dc = tmem + 96u * mt;
-#pragma unroll 1
-        for (int ks = 0; ks < SL / 16; ++ks) {
-          const uint64_t db = umma::desc_noswz(v_addr + (uint32_t)(2 * ks) * 1536u, 1536, 128);
-          const uint32_t aa = a_addr + (uint32_t)(2 * ks) * (KG * 128u) + (uint32_t)(16 * mt) * 128u;
-          mma_bf16(dc, umma::desc_noswz(aa, KG * 128, 128), db, ID_C96, ks != 0);
-          mma_bf16(dc + 32, umma::desc_noswz(aa + (uint32_t)(A_PIECE * 2), KG * 128, 128), db, ID_C64, 1u);
-          if (NA == 3)
-            mma_bf16(dc + 64, umma::desc_noswz(aa + (uint32_t)(2 * A_PIECE * 2), KG * 128, 128), db, ID_C32, 1u);
         }
       }
       umma::commit(&G.bar_c);
@@ -808,7 +790,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         }
       }
       fmask = __ballot_sync(0xffffffffu, fin);
-      if (lane == 0) G.zfin = fmask;  // read by round 2 after the group barrier
       const long long tdec1 = pdec ? clock64() : 0;
       const float* zsp = zsl + (size_t)(par ^ 1) * rs * TS;  // z_it slice (last pass)
       for (unsigned mm = fmask; mm; mm &= mm - 1) {  // my slice of z_it of every finished unit
@@ -834,7 +815,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
   #pragma unroll
       for (int mt = 0; mt < MTC; ++mt) {  // round 1: my TMEM rows of zp (t = lane row) straight to the owner of row t
         float zp[SPT];
-        if constexpr (RF) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+        {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
           float b0[SPT], b1[SPT];
           const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)slot0;
           if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
@@ -842,14 +823,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           umma::ld_wait();
   #pragma unroll
           for (int j = 0; j < SPT; ++j) zp[j] = b1[j] + b0[j];
-        } else {
-          float b0[SPT], b1[SPT], b2[SPT];
-          const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)slot0;
-          if constexpr (SPT == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
-          else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
-          umma::ld_wait();
-  #pragma unroll
-          for (int j = 0; j < SPT; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
         }
         const int t = 128 * mt + lrow;
         if (t < KP) {
@@ -885,7 +858,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         for (int bk = 0; bk < SPT / BR; ++bk) {
           const int sb = slot0 + BR * bk;
           float zp[BR];
-          if constexpr (RF) {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
+          {  // order blocks a0 v0 | a0 v1 + a1 v0, summed smallest first
             float b0[BR], b1[BR];
             const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 64u * mt + (uint32_t)sb;
             if constexpr (BR == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); }
@@ -893,14 +866,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
             umma::ld_wait();
   #pragma unroll
             for (int j = 0; j < BR; ++j) zp[j] = b1[j] + b0[j];
-          } else {
-            float b0[BR], b1[BR], b2[BR];
-            const uint32_t tc = tmem + ((uint32_t)(32 * q) << 16) + 96u * mt + (uint32_t)sb;
-            if constexpr (BR == 16) { umma::ld16(tc, b0); umma::ld16(tc + 32, b1); umma::ld16(tc + 64, b2); }
-            else { umma::ld8(tc, b0); umma::ld8(tc + 32, b1); umma::ld8(tc + 64, b2); }
-            umma::ld_wait();
-  #pragma unroll
-            for (int j = 0; j < BR; ++j) zp[j] = (b2[j] + b1[j]) + b0[j];
           }
           if (t < KP) {
             if (owner == crank) {
@@ -945,7 +910,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         prof[10] += tdec3 - tdec0;
         prof[14] += __popc(fmask);
       }
-      if constexpr (RF) {
+      {  // slots whose z_it is 0 at the next pass (fresh or empty)
         const unsigned zm = __ballot_sync(0xffffffffu, !(G.state[lane] == 1) || G.it[lane] == 0);
         if (lane == 0) G.zmask[par ^ 1] = zm;
       }
@@ -962,7 +927,7 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
         // swizzled inbox/slice accesses and the z-operand stores are bank-conflict free
         const int sg = item / vmine, row = item - sg * vmine, t = r0 + row;
         float v8[8];
-        if constexpr (RF) {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
+        {  // z_{it+1} = z_it + sum_c partial_c (z_it = 0 for fresh or empty slots)
           const uint32_t zm = G.zmask[par] >> (8 * sg);
           const float* zrow = zs_prev + (size_t)row * TS;
           const float4 p0 = *reinterpret_cast<const float4*>(zrow + 4 * ((2 * sg) ^ (row & 7)));
@@ -970,9 +935,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           const float zv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
           for (int i = 0; i < 8; ++i) v8[i] = ((zm >> i) & 1u) ? 0.f : zv[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v8[i] = 0.f;
         }
         {  // fixed summation order c = 0 .. C-1 (results independent of the unrolling)
           int c = 0;
@@ -1001,13 +963,6 @@ adm_tc_kernel(const float* __restrict__ X, const float* __restrict__ A, int64_t 
           }
         }
         stamp(7);
-        if constexpr (!RF) {  // slots finished at this pass restart (refill) or idle with z = 0
-          const uint32_t zf = G.zfin >> (8 * sg);
-          if (zf & 0xFFu) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v8[i] = ((zf >> i) & 1u) ? 0.f : v8[i];
-          }
-        }
         uint4 w0, w1, w2;
         split8(v8, w0, w1, w2);
         const size_t off = (size_t)((t >> 3) * 12 + sg) * 64 + (t & 7) * 8;  // piece p at + 4 p * 64
