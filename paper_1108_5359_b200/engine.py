@@ -510,7 +510,7 @@ class HostPipeline:
                      af=torch.empty((r1 - r0, k), dtype=dt, device="cuda"),
                      ev_h=torch.cuda.Event(), ev_c=torch.cuda.Event())
             self.chunks.append(c)
-        self.ev_start, self.ev_d2h = torch.cuda.Event(), torch.cuda.Event()
+        self.ev_start, self.ev_d2h, self.ev_panel = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
 
     def solve(self, m_host, l_host, s_host):
         """Enqueue one solve; returns (filter stats dict, residual partials).  The caller's
@@ -521,17 +521,19 @@ class HostPipeline:
         code_in = dv.dtype_code(self.m_dev)
         code_f = _lib.F32 if p.filter_dtype == torch.float32 else _lib.F64
         self.ev_start.record(comp)
-        self.h2d.wait_event(self.ev_start)
         self.d2h.wait_event(self.ev_start)
+        # column panel straight from host memory first (the column filter, and so the first L
+        # rows, wait for it; the chunk copies would share the PCIe link with it), column filter
+        _lib.call("l1f_gather", code_in, m_host.data_ptr(), m_host.stride(0), dv.ptr(p.d_row_idx),
+                  len(seed.row_idx), dv.ptr(p.d_comp_cols), len(p.comp_cols), code_f, dv.ptr(self.xc),
+                  self.xc.stride(0), 1, dv.stream())
+        self.ev_panel.record(comp)
+        self.h2d.wait_event(self.ev_panel)
         # H2D of the row chunks (copy engine)
         with torch.cuda.stream(self.h2d):
             for c in self.chunks:
                 self.m_dev[c["r0"]:c["r1"]].copy_(m_host[c["r0"]:c["r1"]], non_blocking=True)
                 c["ev_h"].record(self.h2d)
-        # column panel straight from host memory, column filter
-        _lib.call("l1f_gather", code_in, m_host.data_ptr(), m_host.stride(0), dv.ptr(p.d_row_idx),
-                  len(seed.row_idx), dv.ptr(p.d_comp_cols), len(p.comp_cols), code_f, dv.ptr(self.xc),
-                  self.xc.stride(0), 1, dv.stream())
         zc, _, itc, _, stc = filter_units(self.xc, p.u, p.adm, want_e=False, workspace=p.workspace)
         if p.filter_dtype != p.dtype:
             zc = zc.to(p.dtype)
