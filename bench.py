@@ -461,11 +461,12 @@ def tensor_roofline(plan, seed, itc, itr, t_ms, peaks):
     if plan.filter_dtype != torch.float32 or k <= 16 or k > 224:
         return None
     if k <= 112:
-        kp, pc = 16 * math.ceil(k / 16), 6
+        kp = 16 * math.ceil(k / 16)
     elif k <= 160:
-        kp, pc = 32 * math.ceil(k / 32), 6
+        kp = 32 * math.ceil(k / 32)
     else:
-        kp, pc = 16 * math.ceil(k / 16), 3  # TA: phase c from the 2-piece dictionary, 3 products
+        kp = 16 * math.ceil(k / 16)
+    pc = 3  # residual-form phase c: a0 v0 + a0 v1 + a1 v0 (phase a: the 6 products of 3 x 3 pieces)
     mtc = math.ceil(kp / 128)
     flops = 0.0
     for it_sum, s_units in ((itc, len(seed.row_idx)), (itr, len(seed.col_idx))):
@@ -475,7 +476,7 @@ def tensor_roofline(plan, seed, itc, itr, t_ms, peaks):
     ach = flops / (t_ms * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained", "executed_mma_flops_per_step": flops,
-            "note": "bf16 pieces: 6 products per contraction (3 for the TA variant's phase c), 128-row tiles"}
+            "note": "bf16 pieces: 6 products in phase a, 3 in the residual-form phase c, 128-row tiles"}
 
 
 def run_e2e(mt, plan, args, l_dev, s_dev):
