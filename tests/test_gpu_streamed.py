@@ -176,3 +176,20 @@ def test_streamed_small_k_matches_separate_calls(m, n, r, concurrent, kind):
         assert torch.equal(got["s"], ref["s"])
         r_ref = ref["resid_sq"].cpu().numpy()  # sum(M^2): fp32 partials grouped differently
         np.testing.assert_allclose(got["resid_sq"].cpu().numpy(), r_ref, rtol=1e-6, atol=1e-6 * r_ref[1])
+
+
+@pytest.mark.parametrize("max_iter,beta0,beta_max", [(3, None, None), (25, 0.05, 50.0)])
+def test_streamed_iteration_limits_and_explicit_beta(max_iter, beta0, beta_max):
+    """Units that stop at max_iter and explicit beta0 / beta_max: the overlapped path counts every
+    finished unit the same way (status MAXITER included) and matches the separate calls."""
+    m, n, r = 3000, 2800, 40
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=21)
+    plan = _plan(mt, r)
+    plan.adm = l1pcp.AdmConfig(tol=1e-7, max_iter=max_iter, beta0=beta0, beta_max=beta_max)
+    ref = _solve(mt, plan, streamed=False)
+    got = _solve(mt, plan, streamed=True)
+    assert torch.equal(got["iters_r"], ref["iters_r"])
+    assert torch.equal(got["status_r"], ref["status_r"])
+    assert torch.equal(got["l"], ref["l"]) and torch.equal(got["s"], ref["s"])
+    if max_iter == 3:
+        assert int((got["status_r"] == 2).sum().item()) > 0
