@@ -105,3 +105,24 @@ def test_compute_without_gpu_fails_loudly():
         l1pcp.soft_threshold(np.ones((2, 2)), 0.5)
     with pytest.raises(_lib.NativeUnavailable):
         l1pcp.estimate_rank_and_solve(np.ones((20, 20)), l1pcp.FilterConfig(rank_hint=1))
+
+
+def test_overlapped_entry_points_validate_before_device_work():
+    """The overlapped filter + reconstruction entry points reject inconsistent shapes with
+    L1F_ERR_ARG before touching the device (host-side checks only: runs without a GPU)."""
+    lib = _lib.load()
+    null = None
+    # row units must be the m - s_r non-seed rows
+    rc = lib.l1f_rowfilter_reconstruct_f32(null, 100, 100, 10, null, 10, 10, 1e-7, 1.5, 0.0, 0.0, 100, null, 10,
+                                           null, null, null, null, null, 5, null, null, null, 5, null, null, 10,
+                                           null, 100, 100, 100, null, 100, null, 100, null, null, null)
+    assert rc == _lib.L1F_ERR_ARG
+    rc = lib.l1f_rowfilter_reconstruct_small(null, 100, 100, 10, null, 10, 10, 1e-7, 1.5, 0.0, 0.0, 100, null, 10,
+                                             null, null, null, null, null, 5, null, null, null, 5, null, null, 10,
+                                             null, 100, 100, 100, null, 100, null, 100, null, null, null)
+    assert rc == _lib.L1F_ERR_ARG
+    # leading dimension of the filter panel below the unit length
+    rc = lib.l1f_filter_with_gather_f32(null, 10, 100, 5, null, 10, 10, 1e-7, 1.5, 0.0, 0.0, 100, null, 10, null,
+                                        null, null, _lib.F32, null, 100, null, 0, null, 0, null, 10, 0, null)
+    assert rc == _lib.L1F_ERR_ARG
+    assert "need" in _lib.last_error() or "shape" in _lib.last_error()
