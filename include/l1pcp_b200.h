@@ -220,6 +220,13 @@ int l1f_generate_f32(uint64_t seed, int32_t kind, int64_t m, int64_t n, int32_t 
                      int64_t row0, int64_t rows, float* M, int64_t ldm,
                      float* L0, int64_t ldl0, void* stream);
 
+/* Exact-count sparse part — replaces synth.generate's support and values (synth.py:56-61):
+ * S (dtype L1F_F32/L1F_F64, m*n contiguous, row-major) gets exactly p nonzeros at uniformly random
+ * distinct positions (a radix select of the p smallest Philox keys, on the device), each
+ * U[-magnitude, magnitude).  ValueError-equivalent L1F_ERR_ARG when p > m*n. */
+int l1f_generate_sparse_exact(int dtype, uint64_t seed, int64_t m, int64_t n, int64_t p, double magnitude,
+                              void* S, void* stream);
+
 /* ------------------------------------------------------------------------------------
  * Reductions — `frobenius_norm`, `l1_norm`, `linf_norm`, `l0_count` and the finiteness
  * check of `as_dense` (matcore.py:13-20,41-63).  out (device double[5]):

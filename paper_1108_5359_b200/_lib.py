@@ -83,6 +83,7 @@ SIGNATURES = {
     "l1f_generate_factors_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "l1f_generate_f32": (_int, [_u64, _i32, _i64, _i64, _i32, _f32, _f32, _vp, _vp, _i64, _i64,
                                 _vp, _i64, _vp, _i64, _vp]),
+    "l1f_generate_sparse_exact": (_int, [_int, _u64, _i64, _i64, _i64, _f64, _vp, _vp]),
     "l1f_norms": (_int, [_int, _vp, _i64, _i64, _i64, _f64, _vp, _vp]),
     "l1f_diff_norms": (_int, [_int, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp]),
     "l1f_soft_threshold": (_int, [_int, _vp, _vp, _i64, _f64, _vp]),

@@ -781,3 +781,108 @@ extern "C" int l1f_soft_threshold(int dtype, const void* X, void* Y, int64_t cou
   L1F_CHECK_LAUNCH();
   return L1F_OK;
 }
+
+// ------------------------------------------------------------------------------------
+// Exact-count sparse support — synth.generate's `rng.choice(m*n, size=p, replace=False)` +
+// `uniform(-mag, mag)` (synth.py:56-61): exactly p of the N entries are nonzero, at uniformly
+// random positions.  Entry e gets a unique 64-bit key (Philox draw in the high bits, e in the low
+// `ib` bits); the support is the p smallest keys, found by an 8-pass radix select (8-bit digits,
+// shared-memory histograms, the digit choice made on the device — no host round trip).
+// ------------------------------------------------------------------------------------
+namespace l1f {
+namespace spx {
+constexpr uint64_t kStreamSupport = 5, kStreamValue = 6;
+
+__device__ __forceinline__ uint64_t key_of(uint64_t seed, int64_t e, int ib) {
+  const uint64_t r = philox_draw(seed, kStreamSupport, (uint64_t)e);
+  return ib >= 64 ? (uint64_t)e : (((r >> ib) << ib) | (uint64_t)e);
+}
+
+struct Sel { uint64_t prefix, mask; int64_t rank; };  // rank: 1-based rank still to find
+
+__global__ void sel_init_kernel(Sel* sel, int64_t p) {
+  sel->prefix = 0; sel->mask = 0; sel->rank = p;
+}
+
+__global__ void sel_hist_kernel(uint64_t seed, int64_t N, int ib, int shift, const Sel* __restrict__ sel,
+                                unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t prefix = sel->prefix, mask = sel->mask;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = key_of(seed, e, ib);
+    if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 0xffu], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+__global__ void sel_pick_kernel(int shift, Sel* sel, unsigned long long* hist) {
+  if (threadIdx.x != 0) return;
+  int64_t rank = sel->rank;
+  int d = 0;
+  for (; d < 255; ++d) {
+    const int64_t c = (int64_t)hist[d];
+    if (rank <= c) break;
+    rank -= c;
+  }
+  sel->prefix |= (uint64_t)d << shift;
+  sel->mask |= (uint64_t)0xff << shift;
+  sel->rank = rank;
+  for (int i = 0; i < 256; ++i) hist[i] = 0;
+}
+
+template <typename T>
+__global__ void sparse_write_kernel(uint64_t seed, int64_t N, int ib, const Sel* __restrict__ sel, int64_t p,
+                                    double mag, T* __restrict__ S) {
+  const uint64_t thr = sel->prefix;  // the p-th smallest key
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    T v = T(0);
+    if (p > 0 && key_of(seed, e, ib) <= thr) {
+      const uint64_t b = philox_draw(seed, kStreamValue, (uint64_t)e);
+      const double u = (double)(b >> 11) * 0x1.0p-53;  // [0, 1)
+      v = (T)(mag * (2.0 * u - 1.0));                  // U[-mag, mag)
+      if (v == T(0)) v = (T)(mag * 0x1.0p-53);        // keep the support exact
+    }
+    S[e] = v;
+  }
+}
+}  // namespace spx
+}  // namespace l1f
+
+extern "C" int l1f_generate_sparse_exact(int dtype, uint64_t seed, int64_t m, int64_t n, int64_t p, double magnitude,
+                                         void* S, void* stream) {
+  using namespace l1f::spx;
+  L1F_REQUIRE(dtype == L1F_F32 || dtype == L1F_F64, L1F_ERR_ARG, "generate_sparse: bad dtype");
+  L1F_REQUIRE(m >= 0 && n >= 0 && p >= 0, L1F_ERR_ARG, "generate_sparse: negative shape");
+  const int64_t N = m * n;
+  L1F_REQUIRE(p <= N, L1F_ERR_ARG, "requested %lld sparse entries in a %lldx%lld matrix", (long long)p, (long long)m,
+              (long long)n);
+  L1F_REQUIRE(magnitude >= 0.0, L1F_ERR_ARG, "generate_sparse: magnitude must be nonnegative");
+  if (N == 0) return L1F_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int ib = 0;
+  while (ib < 63 && ((uint64_t)1 << ib) < (uint64_t)N) ++ib;
+  Scratch buf(st);
+  L1F_CUDA_TRY(buf.alloc(sizeof(Sel) + 256 * sizeof(unsigned long long)));
+  Sel* sel = (Sel*)buf.p;
+  unsigned long long* hist = (unsigned long long*)((char*)buf.p + sizeof(Sel));
+  L1F_CUDA_TRY(cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned long long), st));
+  const int g = grid_for(N, 256);
+  if (p > 0) {
+    sel_init_kernel<<<1, 1, 0, st>>>(sel, p);
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      sel_hist_kernel<<<g, 256, 0, st>>>(seed, N, ib, shift, sel, hist);
+      sel_pick_kernel<<<1, 32, 0, st>>>(shift, sel, hist);
+    }
+    L1F_CHECK_LAUNCH();
+  }
+  if (dtype == L1F_F64)
+    sparse_write_kernel<double><<<g, 256, 0, st>>>(seed, N, ib, sel, p, magnitude, (double*)S);
+  else
+    sparse_write_kernel<float><<<g, 256, 0, st>>>(seed, N, ib, sel, p, magnitude, (float*)S);
+  L1F_CHECK_LAUNCH();
+  return L1F_OK;
+}

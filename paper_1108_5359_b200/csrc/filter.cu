@@ -408,6 +408,181 @@ int run(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda
   return rc;
 }
 
+// ---------------------------------------------------------------- any-k kernel (k > 256)
+// One CTA solves one unit at a time; the unit's state (y, e double buffer, v, z, A z) lives in a
+// per-CTA workspace, and the dictionary is read from two padded copies in global memory (row-major
+// for A^T v, transposed for A z) so both contractions are coalesced.  Same recurrence, same
+// sequential FMA order over t (A z) and over rows (A^T v) as the streaming kernel above, so the
+// per-unit arithmetic matches it and is independent of the grid.  The refusal of k > 256 it replaces
+// was a register limit of the streaming kernel, not of the algorithm (l1reg.py:59-137 takes any k).
+constexpr int GT = 256;  // threads per CTA of the any-k kernel
+
+template <typename T>
+__global__ void __launch_bounds__(GT)
+adm_generic_kernel(const T* __restrict__ X, const T* __restrict__ Ap, const T* __restrict__ At,
+                   const T* __restrict__ scale, Params P, T* __restrict__ ws, T* __restrict__ Z, T* __restrict__ E,
+                   int32_t* __restrict__ iters, T* __restrict__ res, uint8_t* __restrict__ status) {
+  const int s = P.s, k = P.k, kp = P.kp, s_pad = P.s_pad;
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  T* y = ws + (int64_t)blockIdx.x * (4 * (int64_t)s_pad + 2 * (int64_t)kp);
+  T* e0 = y + s_pad;
+  T* e1 = e0 + s_pad;
+  T* v = e1 + s_pad;
+  T* z = v + s_pad;
+  T* zn = z + kp;
+  __shared__ T red[GT / 32];
+  __shared__ int fin_s;
+  const T tol = (T)P.tol, rho = (T)P.rho;
+  for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+    const T sc = scale[u];
+    if (!(sc > T(0)) || P.max_iter <= 0) continue;  // written by unit_scale_kernel
+    const T* x = X + u * P.ldx;
+    const T b0 = P.beta0 > 0 ? (T)P.beta0 : recip(sc);
+    const T bmax = P.beta_max > 0 ? (T)P.beta_max : (T)1e7 * b0;
+    const T thresh = tol * sc;
+    T beta_cur = b0, beta_next = b0, inv_next = recip(b0), prev_res = Limits<T>::inf(), r_last = T(0);
+    int it = 0, stalled = 0, buf = 0;
+    uint8_t code = L1F_UNIT_OK;
+    for (int t = tid; t < kp; t += GT) z[t] = T(0);
+    __syncthreads();
+    for (;;) {
+      // phase a + b: rows i
+      T rmax = T(0);
+      const T* e_rd = buf ? e1 : e0;
+      T* e_wr = buf ? e0 : e1;
+      for (int i = tid; i < s; i += GT) {
+        T az = T(0);
+        for (int t = 0; t < kp; ++t) az = fma(At[(int64_t)t * s_pad + i], z[t], az);
+        const T xi = x[i];
+        T yi, d;
+        if (it == 0) {
+          yi = T(0);
+          d = xi;
+        } else {
+          d = xi - az;
+          const T r = d - e_rd[i];
+          rmax = tmax(rmax, tabs(r));
+          yi = y[i] + beta_cur * r;
+        }
+        const T yb = yi * inv_next;
+        const T e = shrink(d + yb, inv_next);
+        v[i] = (xi - e) + yb;
+        y[i] = yi;
+        e_wr[i] = e;
+      }
+      rmax = warp_max(rmax);
+      if (lane == 0) red[warp] = rmax;
+      __syncthreads();
+      if (tid == 0) {
+        T m = T(0);
+        for (int w = 0; w < GT / 32; ++w) m = tmax(m, red[w]);
+        int fin = 0;
+        if (it > 0) {
+          const T rel = tabs(m - prev_res) / tmax(m, Limits<T>::tiny());
+          stalled = (rel < (T)kStallEps) ? stalled + 1 : 0;
+          prev_res = m;
+          r_last = m;
+          if (m <= thresh) { fin = 1; code = L1F_UNIT_OK; }
+          else if (stalled >= kStallIters) { fin = 1; code = L1F_UNIT_STALLED; }
+          else if (it >= P.max_iter) { fin = 1; code = L1F_UNIT_MAXITER; }
+        }
+        fin_s = fin;
+      }
+      __syncthreads();
+      // every thread mirrors the scalar schedule (thread 0 owns the decision)
+      const int fin = fin_s;
+      if (fin) {
+        for (int t = tid; t < k; t += GT) Z[u * P.ldz + t] = z[t];
+        if (E)
+          for (int i = tid; i < s; i += GT) E[u * P.lde + i] = e_rd[i];
+        if (tid == 0) {
+          if (iters) iters[u] = it;
+          if (res) res[u] = r_last;
+          if (status) status[u] = code;
+        }
+        __syncthreads();
+        break;
+      }
+      it += 1;
+      beta_cur = beta_next;
+      T bn = rho * beta_cur;
+      if (bn > bmax) bn = bmax;
+      beta_next = bn;
+      inv_next = recip(bn);
+      buf ^= 1;
+      // phase c: z_{it} = A^T v, sequential over rows
+      for (int t = tid; t < kp; t += GT) {
+        T acc = T(0);
+        for (int i = 0; i < s; ++i) acc = fma(Ap[(int64_t)i * kp + t], v[i], acc);
+        zn[t] = acc;
+      }
+      __syncthreads();
+      for (int t = tid; t < kp; t += GT) z[t] = zn[t];
+      __syncthreads();
+    }
+  }
+}
+
+template <typename T>
+__global__ void transpose_dictionary_kernel(const T* __restrict__ A, int64_t lda, int s, int k, int s_pad, int kp,
+                                            T* __restrict__ At) {
+  const int64_t total = (int64_t)s_pad * kp;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e / s_pad), r = (int)(e % s_pad);
+    At[e] = (r < s && t < k) ? A[(int64_t)r * lda + t] : T(0);
+  }
+}
+
+template <typename T>
+int run_generic(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
+                double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
+                int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
+                bool query, size_t* need) {
+  const int s_pad = (int)ceil_div(s, RC) * RC, kp = (int)ceil_div(k, 32) * 32;
+  const int64_t g64 = std::min<int64_t>(std::max<int64_t>(n_units, 1), (int64_t)num_sms() * 4);
+  const int grid = (int)g64;
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t ap_off = 0;
+  const size_t at_off = al(ap_off + sizeof(T) * (size_t)s_pad * kp);
+  const size_t scale_off = al(at_off + sizeof(T) * (size_t)s_pad * kp);
+  const size_t ws_off = al(scale_off + sizeof(T) * (size_t)(n_units > 0 ? n_units : 1));
+  const size_t total = al(ws_off + sizeof(T) * (size_t)grid * (4 * (size_t)s_pad + 2 * (size_t)kp));
+  if (query) {
+    *need = total;
+    return L1F_OK;
+  }
+  void* owned = nullptr;
+  if (!workspace) {
+    L1F_CUDA_TRY(cudaMallocAsync(&owned, total, st));
+    workspace = owned;
+  } else {
+    L1F_REQUIRE(ws_bytes >= total, L1F_ERR_ARG, "filter: workspace too small (%zu < %zu)", ws_bytes, total);
+  }
+  unsigned char* w = (unsigned char*)workspace;
+  Params P;
+  P.s = s; P.s_pad = s_pad; P.k = k; P.kp = kp;
+  P.n_units = n_units; P.ldx = ldx; P.ldz = ldz; P.lde = lde; P.max_iter = max_iter;
+  P.tol = tol; P.rho = rho; P.beta0 = beta0; P.beta_max = beta_max;
+  T* Ap = (T*)(w + ap_off);
+  T* At = (T*)(w + at_off);
+  T* scale = (T*)(w + scale_off);
+  T* ws = (T*)(w + ws_off);
+  int rc = L1F_OK;
+  do {
+    pad_dictionary_kernel<T><<<256, 256, 0, st>>>(A, lda, s, k, s_pad, kp, Ap);
+    transpose_dictionary_kernel<T><<<256, 256, 0, st>>>(A, lda, s, k, s_pad, kp, At);
+    unit_scale_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(n_units, 8), 65535), 256, 0, st>>>(
+        X, P, scale, Z, E, iters, res, status);
+    if (cudaGetLastError() != cudaSuccess) { rc = L1F_ERR_CUDA; break; }
+    if (max_iter <= 0) break;
+    adm_generic_kernel<T><<<grid, GT, 0, st>>>(X, Ap, At, scale, P, ws, Z, E, iters, res, status);
+    if (cudaGetLastError() != cudaSuccess) { rc = L1F_ERR_CUDA; break; }
+  } while (0);
+  if (rc != L1F_OK) set_error("filter: kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (owned) cudaFreeAsync(owned, st);
+  return rc;
+}
+
 template <typename T>
 int dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
              double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
@@ -420,9 +595,9 @@ int dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_
                      iters, res, status, workspace, ws_bytes, st, query, need);
   switch (kj < 1 ? 1 : kj) {
     L1F_KJ(1) L1F_KJ(2) L1F_KJ(3) L1F_KJ(4) L1F_KJ(5) L1F_KJ(6) L1F_KJ(7) L1F_KJ(8)
-    default:
-      set_error("filter: k = %d exceeds the compiled maximum of 256", k);
-      return L1F_ERR_UNSUPPORTED;
+    default:  // k > 256: the any-k kernel
+      return run_generic<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde,
+                            iters, res, status, workspace, ws_bytes, st, query, need);
   }
 #undef L1F_KJ
 }
