@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-chunks", type=int, default=8, help="row chunks of the pipelined host-buffer solve")
-    p.add_argument("--cpu-sample-units", type=int, default=0, help="units per filter in the CPU sample")
+    p.add_argument("--no-extra", action="store_true", help="skip the cfg5 sub-object and the FP64 API legs")
     return p.parse_args()
 
 
@@ -131,126 +131,102 @@ def measured_peaks():
         return {}
 
 
-# ---------------------------------------------------------------- CPU (oracle) sample
-def cpu_sample(cfgd, seed_np, m_rows, m_cols, n_units, threads):
-    """Time the reference algorithm (numpy oracle) on a bounded sample of the workload:
-    the ADM filter on n_units column units and n_units row units plus the reconstruction
-    of a block of rows; extrapolate to the whole matrix.  Returns dict."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import adm_filter, philox_gen
-
-    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
-    ri, ci = seed_np["row_idx"], seed_np["col_idx"]
-    u, sig, v = seed_np["u"], seed_np["sigma"], seed_np["v"]
-    comp_r = np.setdiff1d(np.arange(m), ri)
-    comp_c = np.setdiff1d(np.arange(n), ci)
-    rng = np.random.default_rng(1)
-    sc = np.sort(rng.choice(comp_c, min(n_units, comp_c.size), replace=False))
-    sr = np.sort(rng.choice(comp_r, min(n_units, comp_r.size), replace=False))
-    x, y = philox_gen.factors(0, cfgd["kind"], m, n, r)
-
-    def blk(rows, cols):
-        return philox_gen.block(0, cfgd["kind"], m, n, r, cfgd["rho_s"], cfgd["magnitude"], rows, cols, x=x,
-                                y=y).astype(np.float64)
-
-    xc = blk(ri, sc)
-    xr = blk(sr, ci).T.copy()
-    recon_rows = max(1, min(m, int(4e6 // n)))
-    mrec = blk(np.arange(recon_rows), np.arange(n))
-
-    def chunked(xp, a):
-        # the reference's fixed 64-column chunks on a thread pool (l1reg.py:183-196)
-        bounds = list(range(0, xp.shape[1], 64)) + [xp.shape[1]]
-        chunks = [(lo, hi) for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]
-
-        def run(c):
-            return adm_filter.solve_units(xp[:, c[0]:c[1]], a, TOL)
-
-        if threads <= 1:
-            return [run(c) for c in chunks]
-        with ThreadPoolExecutor(max_workers=threads) as pool:
-            return list(pool.map(run, chunks))
-
-    t0 = time.perf_counter()
-    outc = chunked(xc, u)
-    outr = chunked(xr, v)
-    t_filter = time.perf_counter() - t0
-    q = np.concatenate([o[0] for o in outc], axis=1)
-    p = np.concatenate([o[0] for o in outr], axis=1)
-    # reconstruction of recon_rows x n: a_i . b_j then S = M - L (l1filter.py:250-254)
-    a_rows = np.tile(p[:, :1].T / sig, (recon_rows, 1))
-    b_cols = np.tile(q[:, :1].T, (n, 1))
-    t0 = time.perf_counter()
-    l = a_rows @ b_cols.T
-    s = mrec - l
-    t_recon = time.perf_counter() - t0
-    del s
-    units_total = comp_c.size + comp_r.size
-    t_est = t_filter / (sc.size + sr.size) * units_total + t_recon / recon_rows * m
-    return {"t_filter_sample": t_filter, "t_recon_sample": t_recon, "units_sampled": int(sc.size + sr.size),
-            "units_total": int(units_total), "recon_rows": recon_rows, "t_est": t_est,
-            "value": m * n / t_est / 1e6}
+# ---------------------------------------------------------------- CPU legs (bench_cpu.py)
+def cpu_leg(cfgd, seed_np, steps, target_s, ref=None, kind=None, validate=True):
+    """Time the reference's own code (oracle/_ref, else the port) on bounded samples of the
+    workload: returns (per-step extrapolated seconds, description dict)."""
+    import bench_cpu
+    if ref is None:
+        ref, kind = bench_cpu.load_reference()
+    wl = bench_cpu.Workload(cfgd, seed=seed_np, ref=ref)
+    probe = 128
+    best, settings = bench_cpu.pick_threads(ref, wl, probe)
+    t_probe = settings[best.label()]["t_est_s"]
+    # size the per-step sample so one step takes about target_s of CPU time
+    per_unit = t_probe / (wl.comp_c.size + wl.comp_r.size)  # incl. the assembly share
+    units = int(max(64, min(wl.comp_c.size, target_s / max(per_unit, 1e-9) / 2)))
+    units = 64 * max(1, units // 64)
+    t_est, t_sample = [], []
+    for i in range(steps):
+        out = bench_cpu.sample_step(ref, wl, units, best, rng_seed=1 + i)
+        t_est.append(out["t_est"])
+        t_sample.append(out["t_sample"])
+    val = None
+    if validate:
+        from paper_1108_5359_b200.synth import BENCHMARK_CONFIGS
+        small = dict(BENCHMARK_CONFIGS[2])
+        if cfgd["name"] != small["name"]:
+            val = bench_cpu.validate_extrapolation(ref, kind, small, min(units, 1024), best)
+    desc = {"kind": kind, "cores": max(best.blas, best.parallelism), "threads": best.label(),
+            "threading_settings": settings,
+            "sample": (f"per step: the reference's filter_columns on {out['units'][0]} and filter_rows on "
+                       f"{out['units'][1]} sampled units, nystrom_complete + assemble + m - l on the "
+                       f"{out['sub_entries']}-entry sub-matrix (seed + sampled rows x cols); extrapolated per unit "
+                       f"to {wl.comp_c.size} + {wl.comp_r.size} units and per entry to {wl.m}x{wl.n}; seed excluded "
+                       f"(as in the GPU arm)"),
+            "sample_seconds_per_step": float(np.mean(t_sample)), "extrapolation_factor":
+                float(np.mean(t_est) / max(np.mean(t_sample), 1e-12)),
+            "extrapolation_check": val, "cpu": bench_cpu.cpu_info()}
+    return t_est, desc
 
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref) on this workload.  With
+    enough host RAM the K timed steps together run the reference pipeline after the seed over the
+    WHOLE matrix once (bench_cpu.full_measure: a measurement, not an extrapolation); otherwise each
+    step is a bounded sample extrapolated per unit / per entry."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import philox_gen, seed_pcp
-
+    import bench_cpu
     cfgd = cfg_of(args.config)
-    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
-    threads = len(os.sched_getaffinity(0))
-    # seed (untimed, as in the GPU arm): regenerate the seed block on the host
-    from oracle.pipeline import sample_indices
-    ss = np.random.SeedSequence(0)
-    ri, ci = sample_indices(m, n, 10 * r, 10 * r, ss.spawn(1)[0])
-    x, y = philox_gen.factors(0, cfgd["kind"], m, n, r)
-    block = philox_gen.block(0, cfgd["kind"], m, n, r, cfgd["rho_s"], cfgd["magnitude"], ri, ci, x=x, y=y)
-    rec = seed_pcp.recover(block.astype(np.float64), tol=TOL)
-    seed_np = {"row_idx": ri, "col_idx": ci, "u": rec[0], "sigma": rec[1], "v": rec[2]}
-    # per-step sample: whole waves of the reference's 64-unit chunks on every host thread (so the
-    # extrapolation sees the full run's parallelism), and about a minute of CPU time in total
-    wave = 64 * threads
-    units = args.cpu_sample_units or wave * max(1, round(default_cpu_units(cfgd) * 5 / max(1, args.steps + args.warmup)
-                                                        / wave))
-    times = []
-    for i in range(args.warmup + args.steps):
-        out = cpu_sample(cfgd, seed_np, m, n, units, threads)
-        if i >= args.warmup:
-            times.append(out["t_est"])
-    t = float(np.mean(times))
-    value = m * n / t / 1e6
+    m, n = cfgd["m"], cfgd["n"]
+    ref, kind = bench_cpu.load_reference()
+    t0 = time.perf_counter()
+    wl = bench_cpu.Workload(cfgd, ref=ref)  # the reference's own seed stage, untimed (as in the GPU arm)
+    t_seed = time.perf_counter() - t0
+    need = 6 * m * n * 8  # M, L, S, completion and the gathers, float64
+    if kind == "reference" and need < 0.6 * _host_ram_bytes():
+        best, settings = bench_cpu.pick_threads(ref, wl, 128)
+        t0 = time.perf_counter()
+        m_full = bench_cpu.host_matrix(wl)
+        t_regen = time.perf_counter() - t0
+        times, detail = bench_cpu.full_measure(ref, wl, m_full, best, args.steps, args.warmup)
+        del m_full
+        t = float(np.sum(times)) / args.steps
+        total = float(np.sum(times))
+        desc = {"kind": kind, "cores": max(best.blas, best.parallelism), "threads": best.label(),
+                "threading_settings": settings,
+                "sample": (f"whole matrix: the {args.steps} timed steps together run the reference's panel gathers, "
+                           f"filter_columns / filter_rows on all {detail['units'][0]} + {detail['units'][1]} units "
+                           f"(1/{args.steps} per step) and nystrom_complete + assemble + m - l on the full {m}x{n} "
+                           f"(last step); seed excluded (as in the GPU arm)"),
+                "measured": detail, "seed_s_untimed": t_seed, "regen_s_untimed": t_regen,
+                "cpu": bench_cpu.cpu_info()}
+        value = m * n / total / 1e6
+    else:
+        steps = args.warmup + args.steps
+        target = float(np.clip(150.0 / max(steps, 1), 1.0, 8.0))
+        t_est, desc = cpu_leg(cfgd, wl.seed, steps, target, ref=ref, kind=kind)
+        t = float(np.mean(t_est[args.warmup:] or t_est))
+        value = m * n / t / 1e6
+        desc["seed_s_untimed"] = t_seed
+    desc.update(value=value, unit=UNIT)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox, BASELINE.json config)",
-            "config": {"workload": workload_name(cfgd), "parallelism": f"cpu threads={threads}"},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{units} column + {units} row ADM units and a {out['recon_rows']}-row "
-                                       f"reconstruction block per step, extrapolated to {out['units_total']} "
-                                       f"units / {m}x{n} entries; seed solved once, untimed"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox, BASELINE.json config, regenerated on host)",
+            "config": {"workload": workload_name(cfgd), "parallelism": f"cpu {desc['threads']}"},
+            "impl": "reference", "cpu_baseline": desc,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
-
-
-def default_cpu_units(cfgd):
-    s, k = 10 * cfgd["r"], cfgd["r"]
-    # ~1 s of numpy per 64-unit chunk at s=1000,k=100; keep the sample near 10-20 s
-    work = s * k
-    return int(max(64, min(2048, 64 * round(2.0e6 * 64 / max(work, 1) / 64))))
 
 
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
-
-    import paper_1108_5359_b200 as l1pcp
-    from paper_1108_5359_b200 import engine
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -260,11 +236,37 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1108_5359_b200 import distributed as pdist
         return pdist.run_bench(args, rank, world, clock_sampler=ClockSampler)
+    from paper_1108_5359_b200 import engine
+    fma_tflops = engine.fma_peak_tflops()
+    line = measure_config(cfg_of(args.config), args, fma_tflops, e2e=not args.no_e2e,
+                          cpu=None if args.no_cpu_baseline else "full", local=local)
+    torch.cuda.empty_cache()
+    if not args.no_extra:
+        # the reference's own contract (numpy float64 in / out, FP64 kernels) through the public call
+        line["fp64_api"] = {f"cfg{c}": fp64_api_leg(cfg_of(c)) for c in (2, 3)}
+        torch.cuda.empty_cache()
+        if args.config != 5:
+            # BASELINE's largest single-GPU config, timed in the same run
+            sub = measure_config(cfg_of(5), argparse.Namespace(**{**vars(args), "steps": min(args.steps, 5)}),
+                                 fma_tflops, e2e=False, cpu=None if args.no_cpu_baseline else "sample",
+                                 local=local)
+            keep = ("metric", "value", "unit", "steps", "warmup", "ms_per_step", "config", "roofline",
+                    "roofline_tensor", "roofline_reconstruct", "generate", "phases_ms", "filter", "value_incl_seed",
+                    "recovery_rel_err", "gpu_launches", "clocks", "cpu_baseline")
+            line["cfg5"] = {k: sub[k] for k in keep if k in sub}
+    print(json.dumps(line))
+    return 0
 
-    cfgd = cfg_of(args.config)
+
+def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
+    """The timed hot path on one GPU for one BASELINE config; returns the JSON line (dict)."""
+    import torch
+
+    import paper_1108_5359_b200 as l1pcp
+    from paper_1108_5359_b200 import engine
+
     m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
     peaks = measured_peaks()
-    fma_tflops = engine.fma_peak_tflops()
 
     # input: Philox on the device
     t0 = time.perf_counter()
@@ -306,7 +308,6 @@ def run_ours(args):
         end.record(stream)
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
-    t_filter = np.mean([e[0].elapsed_time(e[2]) for e in ev_all]) if ev_all else 0.0  # gathers excluded below
     t_filter_only = np.mean([e[1].elapsed_time(e[2]) for e in ev_all])
     streamed = bool(f.get("streamed"))
     if streamed:
@@ -345,28 +346,25 @@ def run_ours(args):
                  + ((f["status_r"] == 1) | (f["status_r"] == 2)).sum().item())
     r2, m2 = rs.cpu().tolist()
 
-    # e2e: host (pinned) M in, L and S out, through the same solve
-    e2e = None
-    if not args.no_e2e and 3 * mt.numel() * mt.element_size() > 0.5 * _host_ram_bytes():
-        e2e = {"value": None, "unit": UNIT, "skipped": "3 pinned host copies of M exceed half the host RAM"}
-    elif not args.no_e2e:
-        e2e = run_e2e(mt, plan, args, l_out, s_out)
-
     # recovery error vs L0 (reported, not gated): regenerate L0 on the device
     rel = recovery_error(cfgd, l_out)
 
-    cpu = None
-    if not args.no_cpu_baseline:
+    # e2e: host (pinned) M in, L and S out, through the public estimate_rank_and_solve
+    e2e_line = None
+    if e2e and 3 * mt.numel() * mt.element_size() > 0.5 * _host_ram_bytes():
+        e2e_line = {"value": None, "unit": UNIT, "skipped": "3 pinned host copies of M exceed half the host RAM"}
+    elif e2e:
+        seed_np = None
+        del l_out, s_out
+        torch.cuda.empty_cache()
+        e2e_line = run_e2e_public(mt, fcfg, args)
+        l_out = s_out = None
+
+    cpu_line = None
+    if cpu:
         seed_np = {"row_idx": seed.row_idx, "col_idx": seed.col_idx, "u": seed.u.cpu().numpy(),
-                   "sigma": seed.sigma.cpu().numpy(), "v": seed.v.cpu().numpy()}
-        threads = len(os.sched_getaffinity(0))
-        wave = 64 * threads  # whole waves of 64-unit chunks on every host thread
-        units = args.cpu_sample_units or wave * max(1, round(default_cpu_units(cfgd) / wave))
-        out = cpu_sample(cfgd, seed_np, m, n, units, threads)
-        cpu = {"value": out["value"], "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{out['units_sampled']} ADM units (numpy oracle, 64-unit chunks on {threads} threads) + "
-                         f"{out['recon_rows']}x{n} reconstruction, extrapolated to {out['units_total']} units / "
-                         f"{m}x{n}"}
+                   "sigma": seed.sigma.cpu().numpy(), "v": seed.v.cpu().numpy(), "seed_l": seed.seed_l.cpu().numpy()}
+        cpu_line = cpu_baseline_leg(cfgd, seed_np, cpu)
 
     small_k = plan.filter_dtype == torch.float64
     if streamed:
@@ -432,11 +430,66 @@ def run_ours(args):
         "recovery_rel_err": rel, "residual": float(np.sqrt(r2 / m2)) if m2 else 0.0,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
-        "cpu_baseline": cpu,
-        "e2e": e2e,
+        "cpu_baseline": cpu_line,
+        "e2e": e2e_line,
     }
-    print(json.dumps(line))
-    return 0
+    del mt, plan, f
+    return line
+
+
+def cpu_baseline_leg(cfgd, seed_np, mode):
+    """cpu_baseline of our line: the reference's own code on the host cores, rank 0 at N=1.
+    mode "full": the whole matrix once when host RAM allows (else a sample); "sample": a bounded
+    sample extrapolated per unit / per entry, with the extrapolation checked on cfg2."""
+    import bench_cpu
+    ref, kind = bench_cpu.load_reference()
+    m, n = cfgd["m"], cfgd["n"]
+    if mode == "full" and kind == "reference" and 6 * m * n * 8 < 0.6 * _host_ram_bytes():
+        wl = bench_cpu.Workload(cfgd, seed=seed_np, ref=ref)
+        best, settings = bench_cpu.pick_threads(ref, wl, 128)
+        m_full = bench_cpu.host_matrix(wl)
+        times, detail = bench_cpu.full_measure(ref, wl, m_full, best, 4, 0)
+        del m_full
+        total = float(np.sum(times))
+        return {"value": m * n / total / 1e6, "unit": UNIT, "kind": kind, "cores": max(best.blas, best.parallelism),
+                "threads": best.label(), "threading_settings": settings,
+                "sample": "whole matrix after the seed (the reference's gathers, filter_columns / filter_rows on all "
+                          "units, nystrom_complete + assemble + m - l), measured once; seed factors = this run's",
+                "measured": detail, "cpu": bench_cpu.cpu_info()}
+    t_est, desc = cpu_leg(cfgd, seed_np, 1, 12.0, ref=ref, kind=kind, validate=True)
+    desc.update(value=m * n / t_est[0] / 1e6, unit=UNIT)
+    return desc
+
+
+def fp64_api_leg(cfgd):
+    """The reference's own contract through the public call: a numpy float64 M in, float64 numpy
+    L, S out (FP64 kernels), FilterConfig(rank_hint=r, tol=1e-7).  Host->device and device->host
+    copies are inside; the seed (t1) is included and reported."""
+    import torch
+
+    import paper_1108_5359_b200 as l1pcp
+    from paper_1108_5359_b200 import engine
+    m, n, r = cfgd["m"], cfgd["n"], cfgd["r"]
+    mt, _, _, _ = engine.generate_matrix(m, n, r, cfgd["rho_s"], cfgd["magnitude"], seed=0, kind=cfgd["kind"])
+    m_np = mt.double().cpu().numpy()
+    del mt
+    torch.cuda.empty_cache()
+    cfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=TOL))
+    l1pcp.estimate_rank_and_solve(m_np[:2000, :2000], cfg)  # warm-up (library start-up)
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        sol = l1pcp.estimate_rank_and_solve(m_np, cfg)
+        el = time.perf_counter() - t0
+        if best is None or el < best[0]:
+            best = (el, sol.stats)
+        del sol
+    el, st = best
+    return {"value_incl_seed": m * n / el / 1e6, "value_excl_seed": m * n / (el - st["t1"]) / 1e6, "unit": UNIT,
+            "elapsed_s": el, "t1_s": st["t1"], "t2_s": st["t2"], "t_assemble_s": st["t_assemble"],
+            "dtype": "f64", "h2d_bytes": m * n * 8, "d2h_bytes": 2 * m * n * 8,
+            "path": "numpy float64 -> as_dense (host) -> device FP64 seed, filters, reconstruction -> numpy L, S"}
 
 
 def ncu_traffic(cfgd):
@@ -479,33 +532,39 @@ def tensor_roofline(plan, seed, itc, itr, t_ms, peaks):
             "note": "bf16 pieces: 6 products in phase a, 3 in the residual-form phase c, 128-row tiles"}
 
 
-def run_e2e(mt, plan, args, l_dev, s_dev):
-    """Same solve with host buffers: pinned M in, L and S out, copies inside the timed region
-    (engine.HostPipeline: zero-copy column panel, chunked H2D / compute / D2H overlap)."""
+def run_e2e_public(mt, fcfg, args):
+    """The same workload end to end through the PUBLIC call a user makes:
+    estimate_rank_and_solve(M) with M a float32 tensor in pinned host memory -> L, S pinned host
+    tensors (l1filter._solve_host_tensor -> engine.HostPipeline: zero-copy seed block and column
+    panel, chunked H2D / compute / D2H overlap).  Copies are inside the timed region.  `value`
+    excludes the seed stage (t1, as the device-resident `value` does; timed on the device from the
+    call's own events), `value_incl_seed` is the whole call by wall clock."""
     import torch
-    from paper_1108_5359_b200 import engine
+
+    import paper_1108_5359_b200 as l1pcp
     m_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
     m_host.copy_(mt)
-    l_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
-    s_host = torch.empty(mt.shape, dtype=mt.dtype, pin_memory=True)
-    pipe = engine.HostPipeline(plan, n_chunks=args.e2e_chunks)
-    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    sol = l1pcp.estimate_rank_and_solve(m_host, fcfg)  # warm-up: pipeline buffers, pinned output pool
+    assert sol.stats.get("path") == "host-pipeline", sol.stats
+    del sol
     steps = max(1, min(args.steps, 3))
-    pipe.solve(m_host, l_host, s_host)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
+    t_solve, t_call = [], []
     for _ in range(steps):
-        _, rs = pipe.solve(m_host, l_host, s_host)
-        r2m2 = rs.cpu()  # device -> host read of the step's result (the residual)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / steps
+        t0 = time.perf_counter()
+        sol = l1pcp.estimate_rank_and_solve(m_host, fcfg)
+        t_call.append(time.perf_counter() - t0)
+        t_solve.append(sol.stats["t2"])  # device events around the pipelined solve (copies included)
+        _ = float(sol.final_residual)   # device -> host read of the step's result
+        del sol
+    ms = float(np.mean(t_solve)) * 1e3
     nbytes = mt.numel() * mt.element_size()
     return {"value": mt.numel() / (ms * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": 2 * nbytes, "ms_per_step": ms, "steps": steps, "chunks": args.e2e_chunks,
-            "path": "pinned host M -> zero-copy column panel + chunked H2D -> filters/factors/reconstruct per "
-                    "chunk -> chunked D2H of L, S (copy/compute overlap, engine.HostPipeline)"}
+            "d2h_bytes_per_step": 2 * nbytes, "ms_per_step": ms, "steps": steps,
+            "value_incl_seed": mt.numel() / float(np.mean(t_call)) / 1e6, "call_s": float(np.mean(t_call)),
+            "api": "paper_1108_5359_b200.estimate_rank_and_solve(pinned float32 host tensor) -> pinned host L, S",
+            "path": "zero-copy seed block + column panel -> chunked H2D -> filters/factors/reconstruct per chunk -> "
+                    "chunked D2H of L, S (engine.HostPipeline)"}
 
 
 def _host_ram_bytes():

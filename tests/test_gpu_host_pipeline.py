@@ -38,3 +38,31 @@ def test_host_pipeline_matches_device_solve(m, n, r, chunks):
     assert torch.equal(stats["iters_r"], ref["iters_r"])
     r_ref = ref["resid_sq"].cpu().numpy()
     np.testing.assert_allclose(rs.cpu().numpy(), r_ref, rtol=1e-9, atol=1e-9 * r_ref[1])
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_public_api_host_tensor_path(pinned):
+    """estimate_rank_and_solve on a float32 HOST tensor (the end-to-end call of bench.py's e2e):
+    L, S come back as host tensors, bitwise equal to the device-resident public call; the seed
+    block and the column panel are read zero-copy from host memory."""
+    m, n, r = 2500, 2200, 25
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=4)
+    cfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=1e-7))
+    dev = l1pcp.estimate_rank_and_solve(mt, cfg)
+    m_host = mt.cpu()
+    if pinned:
+        m_host = m_host.pin_memory()
+    sol = l1pcp.estimate_rank_and_solve(m_host, cfg)
+    assert sol.stats.get("path") == "host-pipeline"
+    assert not sol.l.is_cuda and sol.l.is_pinned() and sol.l.dtype == torch.float32
+    assert torch.equal(sol.l, dev.l.cpu()) and torch.equal(sol.s, dev.s.cpu())
+    assert sol.rank_of_l == dev.rank_of_l == r
+    assert sol.iterations == dev.iterations
+    assert sol.stats["seed_iterations"] == dev.stats["seed_iterations"]
+
+
+def test_public_api_host_tensor_rejects_non_finite():
+    m_host = torch.ones((600, 500), dtype=torch.float32)
+    m_host[3, 4] = float("nan")
+    with pytest.raises(ValueError):
+        l1pcp.estimate_rank_and_solve(m_host, l1pcp.FilterConfig(rank_hint=20))
