@@ -18,6 +18,14 @@
 #include <cstdlib>
 #include <vector>
 
+bool l1f_seed_small_applies(int64_t m, int64_t n);
+int l1f_pcp_small(const double* M, int64_t ldm, int64_t m, int64_t n, double lam, double tol, double beta0,
+                  double rho, double beta_max, int32_t max_iter, double* L, double* S, int32_t* iters_host,
+                  double* residual_host, int32_t* rank_host, int32_t* converged_host, double* beta_final_host,
+                  cudaStream_t st);
+int l1f_svd_small(const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sigma, double* V,
+                  cudaStream_t st);
+
 namespace l1f {
 namespace seed {
 
@@ -194,7 +202,8 @@ static int svt_into(Handles* h, const double* W, int64_t m, int64_t n, double et
   L1F_CUDA_TRY(u.alloc(sizeof(double) * (size_t)m * p));
   L1F_CUDA_TRY(v.alloc(sizeof(double) * (size_t)n * p));
   L1F_CUDA_TRY(sg.alloc(sizeof(double) * (size_t)p));
-  int rc = svd_rowmajor(h, W, m, n, n, u.d(), sg.d(), v.d(), st);
+  int rc = l1f_seed_small_applies(m, n) ? l1f_svd_small(W, m, n, n, u.d(), sg.d(), v.d(), st)
+                                       : svd_rowmajor(h, W, m, n, n, u.d(), sg.d(), v.d(), st);
   if (rc) return rc;
   std::vector<double> sh((size_t)p);
   L1F_CUDA_TRY(cudaMemcpyAsync(sh.data(), sg.p, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, st));
@@ -319,12 +328,10 @@ static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double et
   return L1F_OK;
 }
 
-// ALM-loop SVT: Gram/eigen form for seed-sized and larger matrices (L1F_SEED_SVT=gesvd forces the SVD)
+// ALM-loop SVT for blocks beyond the small-block kernel (seed_small.cu): Gram/eigen form
 static int svt_loop(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
                     cudaStream_t st) {
-  const char* mode = getenv("L1F_SEED_SVT");
-  const bool use_svd = (mode && mode[0] == 'g') || (m < 128 && n < 128);
-  return use_svd ? svt_into(h, W, m, n, eta, out, rank, st) : svt_gram(h, W, m, n, eta, out, rank, st);
+  return svt_gram(h, W, m, n, eta, out, rank, st);
 }
 
 static int spectral_norm(Handles* h, const double* M, int64_t m, int64_t n, int iters, double* out, cudaStream_t st) {
@@ -365,8 +372,9 @@ extern "C" int l1f_svd_f64(const double* W, int64_t m, int64_t n, int64_t ldw, d
                            void* stream) {
   L1F_REQUIRE(m >= 1 && n >= 1 && ldw >= n, L1F_ERR_ARG, "svd: bad shape");
   L1F_REQUIRE(m < INT32_MAX && n < INT32_MAX, L1F_ERR_UNSUPPORTED, "svd: matrix too large");
-  Handles* h;
   cudaStream_t st = (cudaStream_t)stream;
+  if (l1f_seed_small_applies(m, n)) return l1f_svd_small(W, m, n, ldw, U, sigma, V, st);
+  Handles* h;
   int rc = handles(st, h);
   if (rc) return rc;
   return svd_rowmajor(h, W, m, n, ldw, U, sigma, V, st);
@@ -460,8 +468,9 @@ extern "C" int l1f_svd_gram_f64(const double* W, int64_t m, int64_t n, int64_t l
                                 double* V, void* stream) {
   L1F_REQUIRE(m >= 1 && n >= 1 && ldw >= n, L1F_ERR_ARG, "svd_gram: bad shape");
   L1F_REQUIRE(m < INT32_MAX && n < INT32_MAX, L1F_ERR_UNSUPPORTED, "svd_gram: matrix too large");
-  Handles* h;
   cudaStream_t st = (cudaStream_t)stream;
+  if (l1f_seed_small_applies(m, n)) return l1f_svd_small(W, m, n, ldw, U, sigma, V, st);
+  Handles* h;
   int rc = handles(st, h);
   if (rc) return rc;
   return svd_gram(h, W, m, n, ldw, U, sigma, V, st);
@@ -487,8 +496,11 @@ extern "C" int l1f_pcp_f64(const double* M, int64_t m, int64_t n, double lam, do
                            double* beta_final_host, void* stream) {
   L1F_REQUIRE(m >= 1 && n >= 1, L1F_ERR_ARG, "matrix must be nonempty");
   L1F_REQUIRE(rho > 1.0 && tol > 0.0 && lam > 0.0, L1F_ERR_ARG, "pcp: need rho > 1, tol > 0, lam > 0");
-  Handles* h;
   cudaStream_t st = (cudaStream_t)stream;
+  if (l1f_seed_small_applies(m, n))  // one persistent CTA, hand-written Jacobi SVT (seed_small.cu)
+    return l1f_pcp_small(M, n, m, n, lam, tol, beta0, rho, beta_max, max_iter, L, S, iters_host, residual_host,
+                         rank_host, converged_host, beta_final_host, st);
+  Handles* h;
   int rc = handles(st, h);
   if (rc) return rc;
   const int64_t count = m * n;
