@@ -345,6 +345,8 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
     failed = int(((f["status_c"] == 1) | (f["status_c"] == 2)).sum().item()
                  + ((f["status_r"] == 1) | (f["status_r"] == 2)).sum().item())
     r2, m2 = rs.cpu().tolist()
+    if not np.isfinite(r2):  # a timed-out overlapped wait (L1F_OPT_WAIT_TIMEOUT_MS): L, S not trustworthy
+        raise RuntimeError("residual is not finite: an overlapped device wait timed out; no bench line")
 
     # recovery error vs L0 (reported, not gated): regenerate L0 on the device
     rel = recovery_error(cfgd, l_out)

@@ -48,6 +48,24 @@ extern "C" {
 #define L1F_GEN_GAUSSIAN 0  /* L0 = X Y^T, X,Y ~ N(0,1); S0 Bernoulli(rho_s) x U[-mag,mag]  */
 #define L1F_GEN_VIDEO 1     /* L0 = X Y^T, X ~ U[0,1), Y ~ U[0,1)*255/r; S0 moving boxes    */
 
+/* Library options: explicit, process-wide switches of the kernel selection (A/B comparisons and
+ * tests).  The defaults are the production choices; nothing is read from the environment. */
+#define L1F_OPT_FILTER_STREAMING 1  /* 1: every filter call takes the streaming SIMT kernel (default 0) */
+#define L1F_OPT_FILTER_TC 2         /* 0: no tensor-core filter kernel (default 1)                      */
+#define L1F_OPT_TC_GROUPS 3         /* 2: at most two slot groups per CTA; 0: automatic (default)       */
+#define L1F_OPT_RECON_TC 4          /* 0: no tensor-core reconstruction (default 1)                      */
+#define L1F_OPT_RECON_STREAM 5      /* 0: the overlapped row-filter + reconstruction calls decline
+                                       with L1F_ERR_UNSUPPORTED (default 1)                              */
+#define L1F_OPT_RECON_CONCURRENT 6  /* 0: the streamed reconstruction runs only after the filter
+                                       (no concurrent launch on the idle SMs; default 1)                 */
+#define L1F_OPT_GATHER_OVERLAP 7    /* 0: l1f_filter_with_gather_f32 declines (default 1)                */
+#define L1F_OPT_WAIT_TIMEOUT_MS 8   /* bound of the device-side waits of the overlapped calls (default
+                                       10000; 0 = give up at once, tests).  A timed-out wait leaves the
+                                       call's residual NaN; the caller must then recompute the step
+                                       with the separate calls (the Python layer does)               */
+int l1f_set_option(int key, int64_t value);
+int l1f_get_option(int key, int64_t* value_host);
+
 const char* l1f_last_error(void);
 int l1f_version(void);
 /* number of SMs of the current device, written to *out_host */

@@ -52,6 +52,8 @@ _int = ctypes.c_int
 # name -> (restype, argtypes); mirrors include/l1pcp_b200.h
 SIGNATURES = {
     "l1f_last_error": (ctypes.c_char_p, []),
+    "l1f_set_option": (_int, [_int, _i64]),
+    "l1f_get_option": (_int, [_int, _vp]),
     "l1f_version": (_int, []),
     "l1f_sm_count": (_int, [_vp]),
     "l1f_filter_workspace_bytes": (_sz, [_int, _i32, _i32, _i64]),
@@ -95,6 +97,54 @@ SIGNATURES = {
                            _vp, _vp, _vp, _vp]),
     "l1f_fma_peak_probe": (_int, [_i32, _vp, _vp, _vp]),
 }
+
+# library options (include/l1pcp_b200.h L1F_OPT_*): explicit process-wide switches of the kernel
+# selection; the defaults are the production choices
+C_OPTIONS = {"filter_streaming": 1, "filter_tc": 2, "tc_groups": 3, "recon_tc": 4, "recon_stream": 5,
+             "recon_concurrent": 6, "gather_overlap": 7, "wait_timeout_ms": 8}
+# host-side choices of the Python engine: the paired column+row filter call, the streamed form of
+# the sharded step (None = the library's pass model), the rank up to which the filter runs in FP64
+PY_OPTIONS = {"filter_pair": True, "sharded_stream": None, "small_k_fp64": 16}
+
+
+def set_option(name, value):
+    """Set one option (C_OPTIONS: in the library; PY_OPTIONS: in the engine)."""
+    if name in C_OPTIONS:
+        call("l1f_set_option", C_OPTIONS[name], int(value))
+    elif name in PY_OPTIONS:
+        PY_OPTIONS[name] = value
+    else:
+        raise ValueError(f"unknown option {name!r}")
+
+
+def get_option(name):
+    if name in C_OPTIONS:
+        v = ctypes.c_int64(0)
+        call("l1f_get_option", C_OPTIONS[name], ctypes.addressof(v))
+        return int(v.value)
+    if name in PY_OPTIONS:
+        return PY_OPTIONS[name]
+    raise ValueError(f"unknown option {name!r}")
+
+
+class options:
+    """Context manager: ``with _lib.options(recon_concurrent=0): ...`` sets options and restores
+    the previous values on exit (tests and A/B comparisons)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
+
 
 _lock = threading.Lock()
 _lib = None

@@ -26,6 +26,14 @@ static void keep_pool_memory(int dev) {
   }
 }
 
+// process-wide option table (l1f_set_option); index = L1F_OPT_* key
+static constexpr int kNumOptions = 9;
+static int64_t g_options[kNumOptions] = {0, 0, 1, 0, 1, 1, 1, 1, 10000};
+
+int64_t option(int key) {
+  return (key > 0 && key < kNumOptions) ? __atomic_load_n(&g_options[key], __ATOMIC_RELAXED) : 0;
+}
+
 int num_sms() {
   static int cached = 0;
   if (!cached) {
@@ -62,6 +70,19 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, float* sink) 
 using namespace l1f;
 
 extern "C" const char* l1f_last_error(void) { return g_err; }
+
+extern "C" int l1f_set_option(int key, int64_t value) {
+  L1F_REQUIRE(key > 0 && key < kNumOptions, L1F_ERR_ARG, "set_option: unknown option %d", key);
+  L1F_REQUIRE(key != L1F_OPT_WAIT_TIMEOUT_MS || value >= 0, L1F_ERR_ARG, "set_option: timeout must be >= 0");
+  __atomic_store_n(&g_options[key], value, __ATOMIC_RELAXED);
+  return L1F_OK;
+}
+
+extern "C" int l1f_get_option(int key, int64_t* value_host) {
+  L1F_REQUIRE(key > 0 && key < kNumOptions && value_host, L1F_ERR_ARG, "get_option: unknown option %d", key);
+  *value_host = option(key);
+  return L1F_OK;
+}
 extern "C" int l1f_version(void) { return 10000; }
 
 extern "C" int l1f_sm_count(int* out_host) {

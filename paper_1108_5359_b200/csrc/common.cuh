@@ -39,6 +39,7 @@ void set_error(const char* fmt, ...);
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int num_sms();
+int64_t option(int key);  // l1f_set_option values (L1F_OPT_*), defaults when unset
 
 template <typename T> struct Limits;
 template <> struct Limits<float> {

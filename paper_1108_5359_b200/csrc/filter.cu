@@ -64,11 +64,8 @@ template <> struct V4<double> {
 template <typename T>
 __device__ __forceinline__ T recip(T b) { return T(1) / b; }
 
-// L1F_FILTER_KERNEL=streaming forces the streaming kernel (A/B comparisons, tests)
-inline bool force_streaming() {
-  const char* v = getenv("L1F_FILTER_KERNEL");
-  return v && v[0] == 's';
-}
+// L1F_OPT_FILTER_STREAMING forces the streaming kernel (A/B comparisons, tests)
+inline bool force_streaming() { return option(L1F_OPT_FILTER_STREAMING) != 0; }
 
 struct Params {
   int s, s_pad, k, kp;
@@ -615,12 +612,12 @@ template <typename T>
 int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
                        double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
                        int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
-                       bool query, size_t* need);
+                       bool query, size_t* need, l1f::tcf::NotifyHost* nh);
 
 int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
                     double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
                     float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
-                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need, l1f::tcf::NotifyHost* nh);
 
 namespace l1f {
 namespace filt {
@@ -636,7 +633,7 @@ int tc_dispatch<float>(const float* X, int64_t ldx, int s, int64_t n_units, cons
                        float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
                        size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
   return l1f_tc_dispatch(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde, iters,
-                         res, status, workspace, ws_bytes, st, query, need);
+                         res, status, workspace, ws_bytes, st, query, need, nullptr);
 }
 
 // small-k group kernel (filter_small.cu), tensor-core kernel (filter_tc.cu, fp32), resident-state kernel (filter_resident.cu) when a geometry fits, else the streaming kernel
@@ -647,7 +644,7 @@ int select(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
            bool query, size_t* need) {
   if (!force_streaming()) {
     const int rs = l1f_small_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz,
-                                         E, lde, iters, res, status, workspace, ws_bytes, st, query, need);
+                                         E, lde, iters, res, status, workspace, ws_bytes, st, query, need, nullptr);
     if (rs != L1F_ERR_UNSUPPORTED) return rs;
     const int rt = tc_dispatch<T>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde,
                                   iters, res, status, workspace, ws_bytes, st, query, need);

@@ -21,8 +21,9 @@ struct Second {
   int* plan_out = nullptr;  // mode 3: 1 if one grid would run, else 0
 };
 
-// host side: progress-notification targets of the next single-set launch on this thread
-// (l1f_rowfilter_reconstruct_f32), and what that launch did
+// host side: progress-notification targets of a single-set filter launch, passed explicitly by
+// the overlapped calls (l1f_rowfilter_reconstruct_*, l1f_filter_with_gather_f32) down to the
+// launch, and what that launch did
 struct NotifyHost {
   const int64_t* rows = nullptr;    // output row of every unit (strip = row >> 7)
   unsigned* cnt = nullptr;          // per strip: + 1 per (unit, CTA of its cluster) with z written
@@ -30,7 +31,6 @@ struct NotifyHost {
   cudaEvent_t after_prologue = nullptr;  // recorded between the prologue and the main launch
   int cluster = 0, ctas = 0;        // out: cluster size, CTAs of the main launch (0: none)
 };
-extern thread_local NotifyHost* g_notify;
 
 }  // namespace tcf
 }  // namespace l1f

@@ -207,7 +207,8 @@ __global__ void unit_scale_kernel(const T* __restrict__ X, Params P, T* __restri
 template <typename T, int KM, int RPL, int L>
 int launch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol, double rho,
            double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde, int32_t* iters, T* res,
-           uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+           uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st, bool query, size_t* need,
+           tcf::NotifyHost* nh) {
   const size_t scale_bytes = (sizeof(T) * (size_t)(n_units > 0 ? n_units : 1) + 255) & ~(size_t)255;
   const size_t total = scale_bytes + 256;
   if (query) { *need = total; return L1F_OK; }
@@ -238,8 +239,6 @@ int launch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
   T* scale = (T*)workspace;
   int* queue = (int*)((unsigned char*)workspace + scale_bytes);
   int rc = L1F_OK;
-  tcf::NotifyHost* nh = tcf::g_notify;
-  tcf::g_notify = nullptr;
   if (nh) {
     P.nrows = nh->rows;
     P.ncnt = nh->cnt;
@@ -272,12 +271,12 @@ template <typename T>
 int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
                        double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
                        int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
-                       bool query, size_t* need) {
+                       bool query, size_t* need, l1f::tcf::NotifyHost* nh) {
   if (k > 16) return L1F_ERR_UNSUPPORTED;
 #define L1F_SMALL(KM, RPL, L)                                                                                   \
   return l1f::small::launch<T, KM, RPL, L>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, \
                                            Z, ldz, E, lde, iters, res, status, workspace, ws_bytes, st, query,  \
-                                           need)
+                                           need, nh)
   if (k <= 4) {
     if (s <= 64) L1F_SMALL(4, 4, 16);
     if (s <= 128) L1F_SMALL(4, 8, 16);
@@ -305,7 +304,9 @@ int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T*
 
 template int l1f_small_dispatch<float>(const float*, int64_t, int, int64_t, const float*, int64_t, int, double, double,
                                        double, double, int, float*, int64_t, float*, int64_t, int32_t*, float*,
-                                       uint8_t*, void*, size_t, cudaStream_t, bool, size_t*);
+                                       uint8_t*, void*, size_t, cudaStream_t, bool, size_t*,
+                                       l1f::tcf::NotifyHost*);
 template int l1f_small_dispatch<double>(const double*, int64_t, int, int64_t, const double*, int64_t, int, double,
                                         double, double, double, int, double*, int64_t, double*, int64_t, int32_t*,
-                                        double*, uint8_t*, void*, size_t, cudaStream_t, bool, size_t*);
+                                        double*, uint8_t*, void*, size_t, cudaStream_t, bool, size_t*,
+                                        l1f::tcf::NotifyHost*);

@@ -92,7 +92,6 @@ struct Pair {
   unsigned* nres;
 };
 
-thread_local NotifyHost* g_notify = nullptr;
 
 // dynamic shared memory: dictionary pieces, then one region per group (byte offsets)
 struct Layout {
@@ -1069,7 +1068,7 @@ template <int KP, int NG, int NA, bool TA = false>
 int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k, double tol,
            double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz, float* E, int64_t lde,
            int32_t* iters, float* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st, bool query,
-           size_t* need) {
+           size_t* need, NotifyHost* nh = nullptr) {
   const int C = (int)ceil_div(s, SL);
   const int rs = (int)ceil_div(KP, C);
   const Layout Lo = make_layout<KP, NG, NA, TA>(C, rs);
@@ -1095,8 +1094,6 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
   P.tol = tol; P.rho = rho; P.beta0 = beta0; P.beta_max = beta_max;
   float* scale = (float*)workspace;
   int rc = L1F_OK;
-  NotifyHost* nh = g_notify;
-  g_notify = nullptr;
   if (nh) nh->cluster = C;
   unit_scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_units, 8), 65535), 256, 0, st>>>(
       X, P, scale, Z, E, iters, res, status, nh ? nh->rows : nullptr, nh ? nh->cnt : nullptr);
@@ -1122,11 +1119,13 @@ int launch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, 
     const int nclusters = (int)std::min<int64_t>(max_clusters, std::max<int64_t>(1, want));
     cfg.gridDim = dim3((unsigned)(nclusters * C), 1, 1);
     static long long* prof = nullptr;
+#ifdef L1F_DIAG  // diagnostics build only: per-phase cycle counts (tools/, -DL1F_DIAG)
     const char* pe = getenv("L1F_TC_PROF");
     if (pe && pe[0] == '1' && !prof) {
       cudaMallocManaged(&prof, 24 * sizeof(long long));
       memset(prof, 0, 24 * sizeof(long long));
     }
+#endif
     Pair Q = {};
     if (nh) {
       Q.nrows = nh->rows;
@@ -1259,22 +1258,20 @@ int launch_pair(const float* X, int64_t ldx, int s, int64_t n_units, const float
 }  // namespace l1f
 
 // dispatch used by filter.cu (float only): L1F_ERR_UNSUPPORTED when the shape does not fit;
-// L1F_FILTER_TC=0 disables the tensor-core kernel
+// L1F_OPT_FILTER_TC = 0 disables the tensor-core kernel
 int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
                     double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
                     float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
-                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
-  const char* env = getenv("L1F_FILTER_TC");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need, l1f::tcf::NotifyHost* nh) {
+  if (l1f::option(L1F_OPT_FILTER_TC) == 0) return L1F_ERR_UNSUPPORTED;
   using namespace l1f::tcf;
   if (k <= 16 || k > 224 || s > 16 * SL) return L1F_ERR_UNSUPPORTED;
 #define L1F_TC(KP, NG, NA)                                                                                       \
   if (fits<KP, NG, NA>(s))                                                                                        \
     return launch<KP, NG, NA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E, lde,  \
-                              iters, res, status, workspace, ws_bytes, st, query, need)
+                              iters, res, status, workspace, ws_bytes, st, query, need, nh)
   if (k <= 112) {  // three (else two) slot groups, dictionary in 3 pieces; L1F_TC_NG=2 forces two
-    const char* ng = getenv("L1F_TC_NG");
-    if (!(ng && ng[0] == '2')) {
+    if (l1f::option(L1F_OPT_TC_GROUPS) != 2) {
       switch ((int)l1f::ceil_div(k, 16) * 16) {
         case 32: L1F_TC(32, 3, 3); break;
         case 48: L1F_TC(48, 3, 3); break;
@@ -1306,7 +1303,7 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
 #define L1F_TA(KP)                                                                                              \
   if (fits<KP, 1, 2, true>(s))                                                                                   \
     return launch<KP, 1, 2, true>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, E,   \
-                                  lde, iters, res, status, workspace, ws_bytes, st, query, need)
+                                  lde, iters, res, status, workspace, ws_bytes, st, query, need, nh)
   switch ((int)l1f::ceil_div(k, 16) * 16) {
     case 176: L1F_TA(176); break;
     case 192: L1F_TA(192); break;
@@ -1324,8 +1321,7 @@ int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const f
 int l1f_tc_pair_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
                          double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
                          int32_t* iters, float* res, uint8_t* status, const l1f::tcf::Second& two, cudaStream_t st) {
-  const char* env = getenv("L1F_FILTER_TC");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  if (l1f::option(L1F_OPT_FILTER_TC) == 0) return L1F_ERR_UNSUPPORTED;
   using namespace l1f::tcf;
   if (k <= 16 || k > 224 || s > 16 * SL) return L1F_ERR_UNSUPPORTED;
 #define L1F_TCP(KP, NG, NA, TA)                                                                                  \
@@ -1333,8 +1329,7 @@ int l1f_tc_pair_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, co
     return launch_pair<KP, NG, NA, TA>(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, \
                                        iters, res, status, two, st)
   if (k <= 112) {
-    const char* ng = getenv("L1F_TC_NG");
-    if (!(ng && ng[0] == '2')) {
+    if (l1f::option(L1F_OPT_TC_GROUPS) != 2) {
       switch ((int)l1f::ceil_div(k, 16) * 16) {
         case 32: L1F_TCP(32, 3, 3, false); break;
         case 48: L1F_TCP(48, 3, 3, false); break;

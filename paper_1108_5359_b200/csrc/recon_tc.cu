@@ -343,6 +343,7 @@ struct StreamArgs {
   unsigned* split_flag;      // per strip: its A pieces are in global memory
   const int* skip;           // concurrent launch: nonzero = the gate timed out, do nothing
   int* err;                  // a bounded wait timed out (residual -> NaN)
+  unsigned long long timeout_ns;  // bound of every wait (L1F_OPT_WAIT_TIMEOUT_MS)
   unsigned* split_ctr;        // next strip to split
   int ntm;                    // strips
   unsigned long long* dbg;   // L1F_RECON_DEBUG: [launch][items, first claim, last item done, split ns, ready-wait ns,
@@ -381,13 +382,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// bounded wait for *p >= need (a safety net: a wait that cannot end is a bug; after 10 s it
-// gives up and raises *err, which turns the residual into NaN instead of hanging the GPU)
-__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned need, int* err, unsigned sleep_ns) {
+// bounded wait for *p >= need (a safety net: a wait that cannot end is a bug; after timeout_ns
+// (L1F_OPT_WAIT_TIMEOUT_MS) it gives up and raises *err, which turns the residual into NaN instead
+// of hanging the GPU; the Python layer then recomputes the step without overlap)
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned need, int* err, unsigned sleep_ns,
+                                         unsigned long long timeout_ns) {
   if (ld_acquire(p) >= need) return;
   const unsigned long long t0 = globaltimer();
   while (ld_acquire(p) < need) {
-    if (globaltimer() - t0 > 10ull * 1000 * 1000 * 1000) { atomicExch(err, 1); return; }
+    if (globaltimer() - t0 > timeout_ns) { atomicExch(err, 1); return; }
     __nanosleep(sleep_ns);
   }
 }
@@ -545,7 +548,7 @@ recon_stream_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_const
       if (dbg && lane == 0) { atomicAdd(dbg, 1ull); atomicMin(dbg + 1, tw0); }
       const int s = w / SA.ipr, c = w - s * SA.ipr;
       if (lane == 0) {  // the strip's A pieces (split by the splitter warps of some CTA)
-        wait_geq(SA.split_flag + s, 1u, SA.err, 128);
+        wait_geq(SA.split_flag + s, 1u, SA.err, 128, SA.timeout_ns);
         fence_async_global();
         if (dbg) atomicAdd(dbg + 6, globaltimer() - tw0);
       }
@@ -613,7 +616,7 @@ recon_stream_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_const
           const int64_t rows = m - (int64_t)s * BM < BM ? m - (int64_t)s * BM : (int64_t)BM;
           const unsigned need = (unsigned)SA.cluster * (unsigned)(rows - (SA.strip_p0[s + 1] - SA.strip_p0[s]));
           const unsigned long long tw = SA.dbg ? globaltimer() : 0ull;
-          wait_geq(SA.ready + s, need, SA.err, 256);
+          wait_geq(SA.ready + s, need, SA.err, 256, SA.timeout_ns);
           if (SA.dbg) atomicAdd(SA.dbg + 8 * SA.launch_id + 4, globaltimer() - tw);
         }
       }
@@ -874,8 +877,7 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
                        cudaStream_t st) {
   using namespace l1f;
   using namespace l1f::rtc;
-  const char* env = getenv("L1F_RECON_TC");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  if (option(L1F_OPT_RECON_TC) == 0) return L1F_ERR_UNSUPPORTED;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   if ((M && (!al16(M) || ldm % 4)) || (L && (!al16(L) || ldl % 4)) || (S && (!al16(S) || lds % 4)))
     return L1F_ERR_UNSUPPORTED;
@@ -913,9 +915,13 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
     sch.ntn = (int)ceil_div(n, BN);
     sch.ntiles = sch.ntm * sch.ntn;
     const int g = std::min(grid, sch.ntiles);
-    // L1F_RECON_TC_MASK (diagnostics): bit 0 drops M, bit 1 drops L, bit 2 drops S
+    // diagnostics build only (-DL1F_DIAG): L1F_RECON_TC_MASK bit 0 drops M, bit 1 drops L, bit 2 drops S
+#ifdef L1F_DIAG
     const char* mk = getenv("L1F_RECON_TC_MASK");
     const int mask = mk ? atoi(mk) : 0;
+#else
+    const int mask = 0;
+#endif
     static bool attr_set[2] = {false, false};
     auto run = [&](auto kern, size_t smem, int which) {
       if (!attr_set[which]) {
@@ -948,7 +954,7 @@ int l1f_reconstruct_tc(int64_t m, int64_t n, int k, const float* Af, int64_t lda
 int l1f_tc_dispatch(const float* X, int64_t ldx, int s, int64_t n_units, const float* A, int64_t lda, int k,
                     double tol, double rho, double beta0, double beta_max, int max_iter, float* Z, int64_t ldz,
                     float* E, int64_t lde, int32_t* iters, float* res, uint8_t* status, void* workspace,
-                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+                    size_t ws_bytes, cudaStream_t st, bool query, size_t* need, l1f::tcf::NotifyHost* nh);
 
 namespace {
 struct SideStream {
@@ -993,10 +999,7 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
                   (s_c == n || Zc),
               L1F_ERR_ARG,
               "rowfilter_reconstruct: null operand");
-  const char* env = getenv("L1F_RECON_STREAM");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
-  const char* tce = getenv("L1F_RECON_TC");
-  if (tce && tce[0] == '0') return L1F_ERR_UNSUPPORTED;
+  if (option(L1F_OPT_RECON_STREAM) == 0 || option(L1F_OPT_RECON_TC) == 0) return L1F_ERR_UNSUPPORTED;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   if (k <= 16 || k > 224 || !al16(M) || !al16(L) || !al16(S) || ldm % 4 || ldl % 4 || lds % 4 ||
       m >= INT32_MAX / 2 || n >= INT32_MAX / 2 || !encode_fn())
@@ -1051,12 +1054,16 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
   // the reconstruction's prologue (Bf, its pieces, the strips' seed-row offsets) is not needed by
   // the row filter: it runs on the side stream, on the SMs the filter leaves free
   auto prologue = [&](cudaStream_t q) -> int {
-    const char* sy = getenv("L1F_RECON_SYNC");
     auto chk = [&](const char* what) {
+#ifdef L1F_DIAG  // diagnostics build only: synchronise and report after every prologue step
+      const char* sy = getenv("L1F_RECON_SYNC");
       if (sy && sy[0] == '1') {
         cudaError_t e = cudaStreamSynchronize(q);
         fprintf(stderr, "[recon sync] %s: %s\n", what, cudaGetErrorString(e));
       }
+#else
+      (void)what;
+#endif
     };
     chk("before prologue");
     int r = l1f_build_factors(L1F_F32, 0, n, k, nullptr, 0, col_idx, s_c, nullptr, sigma, V64, Zc, ldzc, nullptr, k,
@@ -1076,10 +1083,8 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
     nh.cnt = ready;
     nh.resident = resident;
     nh.after_prologue = side->e0;
-    tcf::g_notify = &nh;
     rc = l1f_tc_dispatch(Xr, ldx, s, n_units, V, ldv, k, tol, rho, beta0, beta_max, max_iter, Zr, ldz, nullptr, s, iters,
-                         res, status, nullptr, 0, st, false, nullptr);
-    tcf::g_notify = nullptr;
+                         res, status, nullptr, 0, st, false, nullptr, &nh);
     if (rc == L1F_OK && nh.cluster == 0) rc = L1F_ERR_UNSUPPORTED;  // the tensor-core launch did not run
   }
   if (rc == L1F_OK && ev_filter_done && cudaEventRecord((cudaEvent_t)ev_filter_done, st) != cudaSuccess) rc = L1F_ERR_CUDA;
@@ -1089,16 +1094,19 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
     StreamArgs SA;
     SA.item_ctr = item_ctr; SA.ready = ready; SA.split_flag = split_flag; SA.skip = nullptr;
     SA.err = reinterpret_cast<int*>(ctr + 3);
+    SA.timeout_ns = (unsigned long long)option(L1F_OPT_WAIT_TIMEOUT_MS) * 1000000ull;
     SA.cluster = nh.cluster; SA.row_idx = row_idx; SA.strip_p0 = strip_p0; SA.U = U; SA.sigma = sigma;
     SA.Zr = Zr; SA.ldzr = ldz; SA.k = k; SA.kp = kp; SA.ah = ah; SA.al = al; SA.inv_a = ia;
     SA.ipr = ipr; SA.cw = cw; SA.n_items = n_items; SA.split_ctr = split_ctr; SA.ntm = ntm;
-    const char* dbe = getenv("L1F_RECON_DEBUG");
     unsigned long long* dbg = nullptr;
+#ifdef L1F_DIAG  // diagnostics build only: per-launch item / wait counters (tools/diag_streamed.py)
+    const char* dbe = getenv("L1F_RECON_DEBUG");
     if (dbe && dbe[0] == '1') {
       cudaMallocManaged(&dbg, sizeof(unsigned long long) * 16);
       for (int i = 0; i < 16; ++i) dbg[i] = (i % 8 == 1) ? ~0ull : 0ull;
       cudaStreamSynchronize(st);
     }
+#endif
     SA.dbg = dbg;
     int next_id = 0;
     auto launch = [&](auto kern, int grid, cudaStream_t stream_, const int* skip_) -> bool {
@@ -1123,6 +1131,7 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
       return false;
     };
     (void)mid;
+#ifdef L1F_DIAG  // diagnostics build only: time the split loop alone
     if (dbe && dbe[0] == '2') {
       unsigned long long* ns = nullptr;
       cudaMallocManaged(&ns, sizeof(unsigned long long));
@@ -1146,10 +1155,10 @@ extern "C" int l1f_rowfilter_reconstruct_f32(
               (double)*ns / 1e3 / ntm);
       cudaFree(ns);
     }
+#endif
     // concurrent part on the SMs the filter leaves free, after the filter is fully resident
     const int spare = nh.ctas > 0 ? nsm - nh.ctas : 0;
-    const char* ce = getenv("L1F_RECON_CONCURRENT");
-    const bool concurrent = spare > 0 && !(ce && ce[0] == '0');
+    const bool concurrent = spare > 0 && option(L1F_OPT_RECON_CONCURRENT) != 0;
     if (concurrent) {
       if (cudaStreamWaitEvent(side->st, side->e0, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
       if (rc == L1F_OK) {
@@ -1215,8 +1224,7 @@ extern "C" int l1f_filter_with_gather_f32(const float* X, int64_t ldx, int32_t s
   using namespace l1f::rtc;
   L1F_REQUIRE(s >= 1 && k >= 1 && n_units >= 0 && ldx >= s && ldz >= k && lda >= k, L1F_ERR_ARG,
               "filter_with_gather: bad filter shape");
-  const char* env = getenv("L1F_GATHER_OVERLAP");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  if (option(L1F_OPT_GATHER_OVERLAP) == 0) return L1F_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
   SideStream* side = side_stream();
   if (!side || n_units == 0 || max_iter <= 0) return L1F_ERR_UNSUPPORTED;
@@ -1227,10 +1235,8 @@ extern "C" int l1f_filter_with_gather_f32(const float* X, int64_t ldx, int32_t s
   if (rc == L1F_OK) {
     nh.resident = resident;
     nh.after_prologue = side->e0;
-    tcf::g_notify = &nh;
     rc = l1f_tc_dispatch(X, ldx, s, n_units, A, lda, k, tol, rho, beta0, beta_max, max_iter, Z, ldz, nullptr, s, iters,
-                         res, status, nullptr, 0, st, false, nullptr);
-    tcf::g_notify = nullptr;
+                         res, status, nullptr, 0, st, false, nullptr, &nh);
     if (rc == L1F_OK && nh.ctas == 0) rc = L1F_ERR_UNSUPPORTED;
   }
   if (rc == L1F_OK) {
@@ -1265,7 +1271,7 @@ template <typename T>
 int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t lda, int k, double tol,
                        double rho, double beta0, double beta_max, int max_iter, T* Z, int64_t ldz, T* E, int64_t lde,
                        int32_t* iters, T* res, uint8_t* status, void* workspace, size_t ws_bytes, cudaStream_t st,
-                       bool query, size_t* need);
+                       bool query, size_t* need, l1f::tcf::NotifyHost* nh);
 
 namespace l1f {
 namespace rtc {
@@ -1276,6 +1282,7 @@ constexpr int SK_RB = 4;                  // rows per ring stage
 constexpr int SK_NS = 8;                  // ring stages (SK_NS - 1 in flight)
 
 struct SmallStreamArgs {
+  unsigned long long timeout_ns;  // bound of every wait (L1F_OPT_WAIT_TIMEOUT_MS)
   unsigned* item_ctr;
   const unsigned* ready;
   const int* skip;
@@ -1320,7 +1327,7 @@ recon_small_stream_kernel(const float* __restrict__ Bf, int64_t ldbf, const floa
     const int s = w / SA.ipr, c = w - s * SA.ipr;
     const int64_t i0 = (int64_t)s * BM, i1 = i0 + BM < m ? i0 + BM : m;
     const int p0 = SA.strip_p0[s], p1 = SA.strip_p0[s + 1];
-    if (tid == 0) wait_geq(SA.ready + s, (unsigned)((i1 - i0) - (p1 - p0)), SA.err, 256);
+    if (tid == 0) wait_geq(SA.ready + s, (unsigned)((i1 - i0) - (p1 - p0)), SA.err, 256, SA.timeout_ns);
     __syncthreads();
     {  // Af row i0 + tid (l1f_build_factors: U row or fp32(Zr row) * fp32(1 / sigma))
       const int64_t i = i0 + tid;
@@ -1440,8 +1447,7 @@ extern "C" int l1f_rowfilter_reconstruct_small(
   L1F_REQUIRE(M && L && S && Zr && (s_r == 0 || (U && row_idx)) && (s_c == 0 || (V64 && col_idx)) && sigma &&
                   (s_c == n || Zc),
               L1F_ERR_ARG, "rowfilter_reconstruct_small: null operand");
-  const char* env = getenv("L1F_RECON_STREAM");
-  if (env && env[0] == '0') return L1F_ERR_UNSUPPORTED;
+  if (option(L1F_OPT_RECON_STREAM) == 0) return L1F_ERR_UNSUPPORTED;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   if (k > 16 || !al16(M) || !al16(L) || !al16(S) || ldm % 4 || ldl % 4 || lds % 4 || m >= INT32_MAX / 2 ||
       n >= INT32_MAX / 2)
@@ -1484,16 +1490,15 @@ extern "C" int l1f_rowfilter_reconstruct_small(
     nh.cnt = ready;
     nh.resident = resident;
     nh.after_prologue = side->e0;
-    tcf::g_notify = &nh;
     rc = l1f_small_dispatch<double>(Xr, ldx, s, n_units, V, ldv, k, tol, rho, beta0, beta_max, max_iter, Zr, ldz, nullptr,
-                                    s, iters, res, status, nullptr, 0, st, false, nullptr);
-    tcf::g_notify = nullptr;
+                                    s, iters, res, status, nullptr, 0, st, false, nullptr, &nh);
     if (rc == L1F_OK && nh.cluster == 0) rc = L1F_ERR_UNSUPPORTED;  // the small-k filter did not run
   }
   if (rc == L1F_OK && ev_filter_done && cudaEventRecord((cudaEvent_t)ev_filter_done, st) != cudaSuccess) rc = L1F_ERR_CUDA;
   if (rc == L1F_OK) {
     SmallStreamArgs SA;
     SA.item_ctr = item_ctr; SA.ready = ready; SA.skip = nullptr; SA.err = err; SA.row_idx = row_idx;
+    SA.timeout_ns = (unsigned long long)option(L1F_OPT_WAIT_TIMEOUT_MS) * 1000000ull;
     SA.strip_p0 = strip_p0; SA.U = U; SA.sigma = sigma; SA.Zr = Zr; SA.ldzr = ldz; SA.k = k; SA.ipr = ipr;
     SA.n_items = n_items;
     auto launch = [&](int grid, cudaStream_t q, const int* skip_) -> bool {
@@ -1522,8 +1527,7 @@ extern "C" int l1f_rowfilter_reconstruct_small(
 #undef L1F_SKS
       return cudaGetLastError() == cudaSuccess;
     };
-    const char* ce = getenv("L1F_RECON_CONCURRENT");
-    const bool concurrent = nh.ctas > 0 && !(ce && ce[0] == '0');
+    const bool concurrent = nh.ctas > 0 && option(L1F_OPT_RECON_CONCURRENT) != 0;
     if (concurrent) {  // one CTA per SM beside the filter's blocks, once they are all resident
       if (cudaStreamWaitEvent(side->st, side->e0, 0) != cudaSuccess) rc = L1F_ERR_CUDA;
       if (rc == L1F_OK) {

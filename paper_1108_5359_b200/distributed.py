@@ -298,16 +298,16 @@ class CudaShardedStep:
         self.streamed = False
         if (self.fdt == torch.float32 and dt == torch.float32 and 16 < self.k <= 224 and len(plan.my_cols) > 0
                 and len(plan.my_rows) > 0 and len(plan.row_idx) == len(plan.col_idx)
-                and os.environ.get("L1F_RECON_STREAM") != "0" and m_local.stride(0) % 4 == 0
+                and self.lib.get_option("recon_stream") != 0 and m_local.stride(0) % 4 == 0
                 and m_local.data_ptr() % 16 == 0):
             import ctypes
             one = ctypes.c_int32(0)
             _lib.call("l1f_filter_pair_plan_f32", len(plan.row_idx), self.k, len(plan.my_cols), len(plan.my_rows),
                       ctypes.addressof(one))
             self.streamed = not one.value
-            force = os.environ.get("L1F_SHARDED_STREAM")  # tests: "1" / "0" overrides the pass model
-            if force in ("0", "1"):
-                self.streamed = force == "1"
+            force = self.lib.PY_OPTIONS["sharded_stream"]  # tests: True / False overrides the pass model
+            if force is not None:
+                self.streamed = bool(force)
         if self.streamed:
             nc, nr = len(plan.my_cols), len(plan.my_rows)
             self.zc = torch.empty((nc, self.k), dtype=torch.float32, device="cuda")
@@ -374,7 +374,7 @@ class CudaShardedStep:
                  dv.stream())
         if events is not None:
             events[0].record()
-        if self.fdt == torch.float32 and self.xc.shape[1] == self.xr.shape[1] and os.environ.get("L1F_FILTER_PAIR") != "0":
+        if self.fdt == torch.float32 and self.xc.shape[1] == self.xr.shape[1] and self.lib.PY_OPTIONS["filter_pair"]:
             # one call for the shard's column and row units (small shards: overlapped drains)
             from .l1reg import filter_units_pair
             (zc, itc, _, stc), (zr, itr, _, st_r) = filter_units_pair(self.xc, self.u, self.xr, self.v, self.adm)

@@ -91,9 +91,10 @@ def recover_seed_device(block, adm=None, rank_tol=1e-6):
     cfg = AdmConfig(lam=lam, tol=adm.tol, beta0=adm.beta0, rho=adm.rho, beta_max=adm.beta_max,
                     max_iter=adm.max_iter)
     l, _, info = solve_pcp_device(block, cfg)
-    # the seed L is exactly low rank (the last SVT), so the Gram route resolves every kept
-    # triplet; L1F_SEED_SVD=gesvd restores the full SVD
-    u, s, v = svd_device(l, gram=os.environ.get("L1F_SEED_SVD", "gram") != "gesvd")
+    # the seed L is exactly low rank (the last SVT): blocks up to 256 are factored by the one-sided
+    # Jacobi kernel (seed_small.cu), larger ones through the Gram route, which resolves every kept
+    # triplet above ~sqrt(eps) * sigma_max; a rank_tol below that needs the full SVD
+    u, s, v = svd_device(l, gram=rank_tol >= 1e-6)
     sh = s.cpu().numpy()
     cutoff = rank_tol * (sh[0] if sh.size else 0.0)
     k = int((sh > cutoff).sum())
@@ -165,7 +166,7 @@ SMALL_K_FP64 = 16
 
 
 def filter_dtype_for(k, dtype):
-    limit = int(os.environ.get("L1F_SMALL_K_FP64", SMALL_K_FP64))
+    limit = int(_lib.PY_OPTIONS["small_k_fp64"])
     return torch.float64 if k <= limit else dtype
 
 
@@ -226,7 +227,7 @@ def filter_stage(plan, mt, events=None):
     if events is not None:
         events[1].record(stream)
     ws = plan.workspace
-    if not plan.want_e and fdt == torch.float32 and xc.shape[1] == xr.shape[1] and os.environ.get("L1F_FILTER_PAIR") != "0":
+    if not plan.want_e and fdt == torch.float32 and xc.shape[1] == xr.shape[1] and _lib.PY_OPTIONS["filter_pair"]:
         # one call for both filters: the library may run them in one grid (overlapped drains)
         from .l1reg import filter_units_pair
         (zc, itc, rc, stc), (zr, itr, rr, st_r) = filter_units_pair(xc, plan.u, xr, plan.v, plan.adm)
@@ -288,7 +289,7 @@ def _streamed_ok(plan, mt):
     """Whether the overlapped row filter + reconstruction (l1f_rowfilter_reconstruct_f32)
     applies: the fp32 tensor-core path over the whole matrix, and the library's pass model
     runs the column and row filters as two launches (one grid wins for small unit sets)."""
-    if os.environ.get("L1F_RECON_STREAM") == "0" or plan.want_e:
+    if not _lib.get_option("recon_stream") or plan.want_e:
         return False
     if not (mt.dtype == torch.float32 and plan.filter_dtype == torch.float32 and 16 < plan.k <= 224):
         return False
@@ -313,7 +314,7 @@ STREAM_SMALL_MIN_ENTRIES = 1 << 24  # below this the small-k reconstruction is t
 def _streamed_small_ok(plan, mt):
     """The small-k form: FP64 filter (k <= 16) on an fp32 matrix large enough that its
     reconstruction is worth running beside the row filter (l1f_rowfilter_reconstruct_small)."""
-    if os.environ.get("L1F_RECON_STREAM") == "0" or plan.want_e:
+    if not _lib.get_option("recon_stream") or plan.want_e:
         return False
     if not (mt.dtype == torch.float32 and plan.filter_dtype == torch.float64 and plan.k <= 16):
         return False

@@ -126,3 +126,21 @@ def test_overlapped_entry_points_validate_before_device_work():
                                         null, null, _lib.F32, null, 100, null, 0, null, 0, null, 10, 0, null)
     assert rc == _lib.L1F_ERR_ARG
     assert "need" in _lib.last_error() or "shape" in _lib.last_error()
+
+
+def test_library_options_are_explicit():
+    """Kernel-selection switches are set through l1f_set_option (no environment reads in the
+    library): defaults, round trip, restore, and the ValueError mapping for an unknown key."""
+    assert _lib.get_option("filter_tc") == 1 and _lib.get_option("recon_stream") == 1
+    assert _lib.get_option("wait_timeout_ms") == 10000
+    with _lib.options(filter_tc=0, tc_groups=2, wait_timeout_ms=5):
+        assert _lib.get_option("filter_tc") == 0 and _lib.get_option("tc_groups") == 2
+        assert _lib.get_option("wait_timeout_ms") == 5
+    assert _lib.get_option("filter_tc") == 1 and _lib.get_option("tc_groups") == 0
+    with pytest.raises(ValueError):
+        _lib.call("l1f_set_option", 99, 1)
+    with pytest.raises(ValueError):
+        _lib.set_option("no_such_option", 1)
+    with _lib.options(filter_pair=False):
+        assert _lib.get_option("filter_pair") is False
+    assert _lib.get_option("filter_pair") is True

@@ -1,6 +1,6 @@
 """GPU: the tensor-core ADM filter (csrc/filter_tc.cu) against the FP64 oracle and the SIMT kernel.
 
-Covers the variants (three slot groups for k <= 112, two with L1F_TC_NG=2; one group with two phase-c M tiles
+Covers the variants (three slot groups for k <= 112, two with the tc_groups=2 option; one group with two phase-c M tiles
 for 112 < k <= 160; one group with the phase-a dictionary in TMEM and the residual-form z step
 for 160 < k <= 224), cluster sizes 1..16, slot refills (many more units than slots) with dead units
 in between, the e output, max_iter status codes, and bitwise independence of unit order.
@@ -32,19 +32,12 @@ def _units(rng, s, k, n, mag=200.0, frac=0.08, scale=5.0):
 
 
 def _run(x, a, tol=1e-7, max_iter=1000, want_e=False, tc=True):
-    old = os.environ.get("L1F_FILTER_TC")
-    os.environ["L1F_FILTER_TC"] = "1" if tc else "0"
-    try:
+    with _lib.options(filter_tc=1 if tc else 0):
         xt = torch.from_numpy(np.ascontiguousarray(x.T, dtype=np.float32)).cuda()
         at = torch.from_numpy(a.astype(np.float32)).cuda()
         out = filter_units(xt, at, l1pcp.AdmConfig(tol=tol, max_iter=max_iter), want_e=want_e)
         torch.cuda.synchronize()
         return [o.cpu() if o is not None else None for o in out]
-    finally:
-        if old is None:
-            del os.environ["L1F_FILTER_TC"]
-        else:
-            os.environ["L1F_FILTER_TC"] = old
 
 
 @pytest.mark.parametrize("s,k,n", [(100, 20, 50), (500, 48, 700), (1000, 100, 2500), (1000, 112, 400),
@@ -115,16 +108,13 @@ def test_tc_results_independent_of_unit_order(k):
 
 @pytest.mark.parametrize("s,k,n,want_e", [(1000, 100, 1500, False), (300, 40, 800, True), (2000, 112, 400, False)])
 def test_tc_three_and_two_slot_groups_bitwise_equal(s, k, n, want_e):
-    # k <= 112 runs three slot groups per CTA (x in TMEM, 8-slot blocks); L1F_TC_NG=2 forces the
+    # k <= 112 runs three slot groups per CTA (x in TMEM, 8-slot blocks); option tc_groups=2 forces the
     # two-group layout.  A unit's arithmetic does not depend on its group or slot.
     rng = np.random.default_rng(s + k)
     a, x = _units(rng, s, k, n)
     three = _run(x, a, want_e=want_e)
-    os.environ["L1F_TC_NG"] = "2"
-    try:
+    with _lib.options(tc_groups=2):
         two = _run(x, a, want_e=want_e)
-    finally:
-        del os.environ["L1F_TC_NG"]
     for f, p in zip(three, two):
         if f is not None:
             assert torch.equal(f, p)

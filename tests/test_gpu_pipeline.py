@@ -267,7 +267,7 @@ def test_sharded_timed_step_matches_single_gpu_solve(m, n, r, stream, monkeypatc
         seed_rows = pdist.gather_seed_rows(mt, plan)
         u, sig, v, _ = pdist.seed_factors(seed_rows, plan, pdist.CudaBackend(), adm)
         if stream is not None:  # the paired-filter step, or the streamed one (filter + reconstruction)
-            monkeypatch.setenv("L1F_SHARDED_STREAM", stream)
+            monkeypatch.setitem(_lib.PY_OPTIONS, "sharded_stream", stream == "1")
         stepper = pdist.CudaShardedStep(mt, plan, adm, u, sig, v)
         if stream is not None:
             assert stepper.streamed == (stream == "1")

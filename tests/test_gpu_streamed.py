@@ -17,26 +17,20 @@ import pytest
 import torch
 
 import paper_1108_5359_b200 as l1pcp
-from paper_1108_5359_b200 import engine
+from paper_1108_5359_b200 import _lib, engine
 
 pytestmark = pytest.mark.gpu
 
 
 def _solve(mt, plan, streamed, concurrent=True):
     old = engine._streamed_ok
-    env = os.environ.get("L1F_RECON_CONCURRENT")
     try:
         engine._streamed_ok = (lambda p, t: True) if streamed else (lambda p, t: False)
-        if not concurrent:
-            os.environ["L1F_RECON_CONCURRENT"] = "0"
-        f = engine.solve_step(plan, mt)
-        torch.cuda.synchronize()
+        with _lib.options(recon_concurrent=1 if concurrent else 0):
+            f = engine.solve_step(plan, mt)
+            torch.cuda.synchronize()
     finally:
         engine._streamed_ok = old
-        if env is None:
-            os.environ.pop("L1F_RECON_CONCURRENT", None)
-        else:
-            os.environ["L1F_RECON_CONCURRENT"] = env
     assert f["streamed"] == streamed
     return f
 
@@ -121,33 +115,26 @@ def test_streamed_shapes(m, n, r):
 
 
 def test_streamed_library_refusal_falls_back(monkeypatch):
-    """If the library declines the overlapped calls (here: L1F_RECON_STREAM / L1F_GATHER_OVERLAP
+    """If the library declines the overlapped calls (here: the recon_stream / gather_overlap options
     switched off underneath a forced streamed plan) solve_step falls back to the separate calls."""
     m, n, r = 3000, 2800, 40
     mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=12)
     plan = _plan(mt, r)
     ref = _solve(mt, plan, streamed=False)
-    monkeypatch.setenv("L1F_RECON_STREAM", "0")
-    monkeypatch.setenv("L1F_GATHER_OVERLAP", "0")
-    got = _solve(mt, plan, streamed=True)
+    with _lib.options(recon_stream=0, gather_overlap=0):
+        got = _solve(mt, plan, streamed=True)
     assert torch.equal(got["l"], ref["l"]) and torch.equal(got["s"], ref["s"])
 
 
 def _solve_small(mt, plan, streamed, concurrent=True):
     old = engine._streamed_small_ok
-    env = os.environ.get("L1F_RECON_CONCURRENT")
     try:
         engine._streamed_small_ok = (lambda p, t: True) if streamed else (lambda p, t: False)
-        if not concurrent:
-            os.environ["L1F_RECON_CONCURRENT"] = "0"
-        f = engine.solve_step(plan, mt)
-        torch.cuda.synchronize()
+        with _lib.options(recon_concurrent=1 if concurrent else 0):
+            f = engine.solve_step(plan, mt)
+            torch.cuda.synchronize()
     finally:
         engine._streamed_small_ok = old
-        if env is None:
-            os.environ.pop("L1F_RECON_CONCURRENT", None)
-        else:
-            os.environ["L1F_RECON_CONCURRENT"] = env
     return f
 
 
@@ -193,3 +180,25 @@ def test_streamed_iteration_limits_and_explicit_beta(max_iter, beta0, beta_max):
     assert torch.equal(got["l"], ref["l"]) and torch.equal(got["s"], ref["s"])
     if max_iter == 3:
         assert int((got["status_r"] == 2).sum().item()) > 0
+
+
+def test_wait_timeout_recomputes_step():
+    """A timed-out device wait of the overlapped row filter + reconstruction (forced here with a
+    zero bound, so every wait that is not already satisfied gives up) leaves a NaN residual; the
+    public call recomputes the step with the separate calls and returns the same L and S (ADVICE r1:
+    recon_tc.cu wait_geq)."""
+    m, n, r = 6000, 5000, 60
+    mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=21)
+    cfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=1e-7))
+    old = engine._streamed_ok
+    try:
+        engine._streamed_ok = lambda p, t: True
+        ref = l1pcp.estimate_rank_and_solve(mt, cfg)
+        assert "overlap_retry" not in ref.stats
+        with _lib.options(wait_timeout_ms=0):
+            got = l1pcp.estimate_rank_and_solve(mt, cfg)
+    finally:
+        engine._streamed_ok = old
+    assert got.stats.get("overlap_retry") is True
+    assert torch.equal(got.l, ref.l) and torch.equal(got.s, ref.s)
+    assert got.final_residual == ref.final_residual
