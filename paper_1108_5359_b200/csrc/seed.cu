@@ -4,9 +4,12 @@
 //   spectral_norm_est. pcp_adm.py:69-87    (25-step power iteration from the all-ones vector)
 //   svd / svt_with_rank matcore.py:73-105  (thin SVD; singular value thresholding)
 //
-// The SVD itself is cuSOLVER's gesvd (a library factorisation, run once per ALM
-// iteration on the s x s seed); everything around it — the fused shrink/residual/dual
-// kernels, the deterministic reductions and the rank-k SVT product — is ours.  The seed
+// Blocks with min(m, n) <= 256 (every seed up to rank 25, the reference's test sizes) never reach
+// this file's library path: l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 hand them to the one-CTA
+// Jacobi kernels of seed_small.cu (no cuSOLVER, no host round trip).  Larger blocks (the rank-50
+// to rank-200 seeds of configs 2, 3 and 5, the full-matrix ADM) use cuSOLVER here: syevd on the
+// Gram matrix inside the ALM loop, gesvd for the public full SVD; the fused shrink/residual/dual
+// kernels, the deterministic reductions and the rank-k SVT products around them are ours.  The seed
 // runs in FP64: its factors must pass the reference's orthonormality check
 // (l1reg.py:48-56, 1e-8) before they are cast to FP32 for the filter.
 #include "common.cuh"
@@ -234,8 +237,10 @@ static int svt_into(Handles* h, const double* W, int64_t m, int64_t n, double et
 // W^T W = V diag(sigma^2) V^T (or W W^T = U diag(sigma^2) U^T when m < n), then
 // out = W V_k diag(1 - eta/sigma_k) V_k^T.  Squaring the spectrum costs relative accuracy only in
 // singular values far below sigma_max, whose SVT contribution (sigma - eta) is absolutely tiny, so
-// the thresholded matrix matches the SVD form to ~eps * sigma_max per entry; the seed's final
-// rank-revealing factorisation still uses the SVD (svd_rowmajor).
+// the thresholded matrix matches the SVD form to ~eps * sigma_max per entry.  The seed's final
+// rank-revealing factorisation (engine.recover_seed_device) takes the Gram route too (svd_gram) when
+// its rank cut is >= 1e-6 of sigma_max, which every kept triplet clears by orders of magnitude; a
+// smaller rank_tol takes the SVD (svd_rowmajor).
 __global__ void scale_rows_cm_kernel(double* __restrict__ T, int64_t rows, int64_t cols, int64_t ld,
                                      const double* __restrict__ c) {
   // column-major T (rows x cols): row j scaled by c[j]
