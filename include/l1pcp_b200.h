@@ -63,6 +63,8 @@ extern "C" {
                                        10000; 0 = give up at once, tests).  A timed-out wait leaves the
                                        call's residual NaN; the caller must then recompute the step
                                        with the separate calls (the Python layer does)               */
+#define L1F_OPT_SMALL_LANES 9       /* lanes per unit of the k <= 10 filter kernel: 0 auto (8 for s <= 104),
+                                       16 or 32                                                          */
 int l1f_set_option(int key, int64_t value);
 int l1f_get_option(int key, int64_t* value_host);
 

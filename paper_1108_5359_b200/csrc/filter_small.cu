@@ -286,6 +286,9 @@ int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T*
     if (s <= 128) L1F_SMALL(8, 8, 16);
     if (s <= 256) L1F_SMALL(8, 8, 32);
   } else if (k <= 10) {  // configs 1 and 4 (k = 10, s = 100): exact width, 8-lane groups
+    const int64_t lanes = l1f::option(L1F_OPT_SMALL_LANES);
+    if (s <= 112 && lanes == 16) L1F_SMALL(10, 7, 16);
+    if (s <= 128 && lanes == 32) L1F_SMALL(10, 4, 32);
     if (s <= 104) L1F_SMALL(10, 13, 8);
     if (s <= 128) L1F_SMALL(10, 8, 16);
     if (s <= 256) L1F_SMALL(10, 8, 32);
