@@ -89,11 +89,24 @@ def _all_gather_rows(local, counts, group=None):
     return torch.cat([out[g * hmax:g * hmax + c] for g, c in enumerate(counts)], dim=0)
 
 
-def gather_seed_rows(m_local, plan, group=None):
-    """Exchange 1: M[row_idx, :] on every rank (each rank contributes the seed rows it owns)."""
-    local = m_local[torch.as_tensor(plan.row_idx[plan.my_seed_pos] - plan.r0, device=m_local.device)]
+def gather_seed_block(m_local, plan, backend, group=None):
+    """Exchange 0 (once per solve, before the timed steps): the s_r x s_c seed block
+    M[row_idx, col_idx] (sample_submatrix, l1filter.py:73-87) on rank 0 only.  Each rank gathers the
+    seed rows it owns at the seed columns (P_g x s_c, an l1f_gather) and rank 0 collects the blocks
+    with one gather (padded to the largest P_g): s_r * s_c * 4 bytes in total, <= 16 MB at config 5,
+    instead of whole seed rows on every rank.  Returns the block on rank 0, None elsewhere."""
     counts = [int((plan.seed_owner == g).sum()) for g in range(plan.world)]
-    return _all_gather_rows(local, counts, group)
+    local = backend.row_panel(m_local, plan.row_idx[plan.my_seed_pos] - plan.r0, plan.col_idx)  # (P_me, s_c)
+    if plan.world == 1:
+        return local
+    hmax = max(max(counts), 1)
+    pad = local.new_zeros((hmax, local.shape[1]))
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(plan.world)] if plan.rank == 0 else None
+    dist.gather(pad, gather_list=bufs, dst=0, group=group)
+    if plan.rank != 0:
+        return None
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
 
 
 def exchange_column_panel(m_local, plan, backend, group=None, out=None):
@@ -123,14 +136,14 @@ def exchange_column_panel(m_local, plan, backend, group=None, out=None):
     return torch.cat(blocks, dim=1, out=out)
 
 
-def seed_factors(seed_rows, plan, backend, adm, rank_tol=1e-6, group=None):
-    """Exchange 2: rank 0 solves the seed PCP, U / sigma / V are broadcast."""
-    dev = seed_rows.device
+def seed_factors(seed_block, plan, backend, adm, rank_tol=1e-6, group=None, device=None):
+    """Exchange 2: rank 0 solves the seed PCP on the gathered block, U / sigma / V are broadcast
+    (<= 6.4 MB at config 5)."""
+    dev = seed_block.device if seed_block is not None else device
     k_buf = torch.zeros(1, dtype=torch.int64, device=dev)
     pcp_it = 0
     if plan.rank == 0:
-        block = seed_rows[:, torch.as_tensor(plan.col_idx, device=dev)]
-        u, sig, v, pcp_it = backend.seed(block, adm, rank_tol)
+        u, sig, v, pcp_it = backend.seed(seed_block, adm, rank_tol)
         k_buf[0] = sig.shape[0]
     dist.broadcast(k_buf, 0, group=group)
     k = int(k_buf.item())
@@ -175,8 +188,8 @@ def solve_from_seed(m_local, plan, backend, adm, u, sig, v, group=None):
 
 def solve_sharded(m_local, plan, backend, adm, rank_tol=1e-6, group=None):
     """Whole distributed solve (seed included).  Returns (L_local, S_local, info)."""
-    seed_rows = gather_seed_rows(m_local, plan, group)
-    u, sig, v, pcp_it = seed_factors(seed_rows, plan, backend, adm, rank_tol, group)
+    block = gather_seed_block(m_local, plan, backend, group)
+    u, sig, v, pcp_it = seed_factors(block, plan, backend, adm, rank_tol, group, device=m_local.device)
     l_local, s_local, info = solve_from_seed(m_local, plan, backend, adm, u, sig, v, group)
     info["pcp_iterations"] = pcp_it
     return l_local, s_local, info
@@ -429,11 +442,11 @@ def run_bench(args, rank, world, clock_sampler=None):
     # seed (t1, outside the timed steps as on one GPU): rank 0 solves, factors broadcast
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    seed_rows = gather_seed_rows(m_local, plan)
-    u, sig, v, _ = seed_factors(seed_rows, plan, backend, adm)
+    block = gather_seed_block(m_local, plan, backend)
+    u, sig, v, _ = seed_factors(block, plan, backend, adm, device=m_local.device)
     torch.cuda.synchronize()
     t1 = time.perf_counter() - t0
-    del seed_rows
+    del block
     stepper = CudaShardedStep(m_local, plan, adm, u, sig, v)
     for _ in range(max(3, args.warmup)):
         stepper.step(m_local)
@@ -500,8 +513,8 @@ def run_bench(args, rank, world, clock_sampler=None):
                 "data": "synthetic (Philox, row shards generated per rank)",
                 "config": {"workload": f"{cfgd['name']}: {m}x{n} r={r}", "m": m, "n": n, "rank": r,
                            "parallelism": f"row-sharded x{world}",
-                           "collectives": "all-gather seed rows, all-gather Q~, all-reduce stats (NCCL); seed factors "
-                                          "broadcast once",
+                           "collectives": "per step: all-to-all of the column panel, all-gather Q~, all-reduce "
+                                          "stats (NCCL); once: seed block gathered to rank 0, seed factors broadcast",
                            "l2": "inputs larger than L2 (row block %.2f GB per GPU)" % (nbytes / world / 1e9)},
                 "roofline": {"bound": "fp32", "kernel": "adm_tc_kernel (column + row filters, max over ranks)",
                              "achieved": ach, "peak": fma * world, "unit": "TFLOP/s", "frac": ach / (fma * world),

@@ -264,8 +264,8 @@ def test_sharded_timed_step_matches_single_gpu_solve(m, n, r, stream, monkeypatc
     try:
         ri, ci = engine.sample_indices(m, n, 10 * r, 10 * r, np.random.SeedSequence(0).spawn(1)[0])
         plan = pdist.ShardPlan(m, n, 0, 1, ri, ci)
-        seed_rows = pdist.gather_seed_rows(mt, plan)
-        u, sig, v, _ = pdist.seed_factors(seed_rows, plan, pdist.CudaBackend(), adm)
+        block = pdist.gather_seed_block(mt, plan, pdist.CudaBackend())
+        u, sig, v, _ = pdist.seed_factors(block, plan, pdist.CudaBackend(), adm)
         if stream is not None:  # the paired-filter step, or the streamed one (filter + reconstruction)
             monkeypatch.setitem(_lib.PY_OPTIONS, "sharded_stream", stream == "1")
         stepper = pdist.CudaShardedStep(mt, plan, adm, u, sig, v)
