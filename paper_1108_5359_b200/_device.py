@@ -56,10 +56,24 @@ def as_device(a, keep_f32=True):
     return torch.from_numpy(arr).cuda(), True
 
 
+# host arrays at least this large (elements) take the parallel host paths below
+BIG_HOST = 1 << 22
+
+
 def to_host_if(t, host):
+    """A new float64 numpy array for host callers (the reference returns fresh numpy arrays).
+    Large results are copied into a numpy buffer whose pages were first touched on all host cores
+    (first-touch page faults of a fresh multi-GB allocation otherwise cost more than the copy)."""
     if not host:
         return t
-    return t.detach().to("cpu", torch.float64).numpy()
+    t = t.detach()
+    if t.numel() < BIG_HOST:
+        return t.to("cpu", torch.float64).numpy()
+    out = np.empty(tuple(t.shape), dtype=np.float64)
+    ho = torch.from_numpy(out)
+    ho.zero_()  # parallel first touch
+    ho.copy_(t if t.dtype == torch.float64 else t.to(torch.float64))
+    return out
 
 
 def empty(shape, dtype=None, like=None):

@@ -33,9 +33,14 @@ def as_dense(a):
     arr = np.asarray(a, dtype=np.float64)
     if arr.ndim != 2:
         raise ValueError(f"expected a 2-D matrix, got ndim={arr.ndim}")
-    if not np.isfinite(arr).all():
+    arr = np.ascontiguousarray(arr)
+    if arr.size >= dv.BIG_HOST:  # the same check on all host cores (torch's parallel CPU kernels)
+        finite = bool(dv.torch.isfinite(dv.torch.from_numpy(arr)).all())
+    else:
+        finite = bool(np.isfinite(arr).all())
+    if not finite:
         raise ValueError("matrix contains non-finite entries")
-    return np.ascontiguousarray(arr)
+    return arr
 
 
 @dataclass(frozen=True)
