@@ -38,8 +38,10 @@ struct Params {
 template <typename T>
 __device__ __forceinline__ T shfl_xor(unsigned mask, T v, int o) { return __shfl_xor_sync(mask, v, o); }
 
-template <typename T, int KM, int RPL, int L>
-__global__ void __launch_bounds__(128)
+// <= 192 registers: two 128-thread blocks plus the 128-thread reconstruction CTA that
+// l1f_rowfilter_reconstruct_small runs beside them fit one SM's register file
+template <typename T, int KM, int RPL, int L, bool WE>
+__global__ void __maxnreg__(192)
 adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, const T* __restrict__ scale, Params P,
                  int* __restrict__ queue, T* __restrict__ Z, T* __restrict__ E, int32_t* __restrict__ iters,
                  T* __restrict__ res_out, uint8_t* __restrict__ status) {
@@ -87,15 +89,40 @@ adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, 
       l[i] = T(0);
     }
     T z[KM];
-#pragma unroll
-    for (int t = 0; t < KM; ++t) z[t] = T(0);
-
     T prev = Limits<T>::inf(), res = T(0);
     int stalled = 0, it = 0;
     uint8_t code = L1F_UNIT_MAXITER;
+    {
+      // ---- first pass (z = 0, y = 0): start iteration 1, peeled so the steady-state pass has no
+      // "fresh" branches.  Same values as the general pass with A z = 0, y = 0.
+      T acc[KM];
+#pragma unroll
+      for (int t = 0; t < KM; ++t) acc[t] = T(0);
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const T* arow = As + (gl + L * i) * AST;
+        const T w = x[i];
+        const T sl = w > T(0) ? tn : -tn;
+        const T v = tabs(w) > tn ? sl : w;  // = l for the first iteration
+        l[i] = v;
+#pragma unroll
+        for (int t = 0; t < KM; ++t) acc[t] = fma(arow[t], v, acc[t]);
+      }
+#pragma unroll
+      for (int o = L / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < KM; ++t) acc[t] += shfl_xor(gmask, acc[t], o);
+      it = 1;
+      bcur = bnext;
+      T bn = rho * bcur;
+      if (bn > bmax) bn = bmax;
+      bnext = bn;
+      tn = T(1) / bn;
+#pragma unroll
+      for (int t = 0; t < KM; ++t) z[t] = acc[t];
+    }
     for (;;) {
-      // ---- one fused pass: finish iteration `it` (it > 0), start iteration it + 1
-      const bool fresh = it == 0;
+      // ---- one fused pass: finish iteration `it`, start iteration it + 1
       T acc[KM];
 #pragma unroll
       for (int t = 0; t < KM; ++t) acc[t] = T(0);
@@ -110,22 +137,16 @@ adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, 
         T azv = T(0);
 #pragma unroll
         for (int t = 0; t < KM; ++t) azv = fma(a[t], z[t], azv);
-        T yv = y[i];
-        if (fresh) {
-          azv = T(0);
-          yv = T(0);
-        } else {
-          if (E != nullptr && row < P.s) E[u * P.lde + row] = x[i] - l[i];  // e_it
-          const T r = l[i] - azv;
-          m = tmax(m, tabs(r));
-          yv = fma(bcur, r, yv);
-        }
+        if (WE && row < P.s) E[u * P.lde + row] = x[i] - l[i];  // e_it
+        const T r = l[i] - azv;
+        m = tmax(m, tabs(r));
+        const T yv = fma(bcur, r, y[i]);
         const T yb = yv * tn;
         const T w = (x[i] - azv) + yb;
         const bool sup = tabs(w) > tn;
-        const T sg = w > T(0) ? T(1) : T(-1);
-        l[i] = sup ? (azv - yb) + sg * tn : x[i];
-        const T v = sup ? azv + sg * tn : x[i] + yb;
+        const T sgt = w > T(0) ? tn : -tn;
+        l[i] = sup ? (azv - yb) + sgt : x[i];
+        const T v = sup ? azv + sgt : x[i] + yb;
         y[i] = yv;
 #pragma unroll
         for (int t = 0; t < KM; ++t) acc[t] = fma(a[t], v, acc[t]);
@@ -137,7 +158,7 @@ adm_small_kernel(const T* __restrict__ X, const T* __restrict__ A, int64_t lda, 
         m = tmax(m, shfl_xor(gmask, m, o));
       }
       bool fin = false;
-      if (!fresh) {
+      {
         const T rel = tabs(m - prev) / tmax(m, Limits<T>::tiny());
         stalled = (rel < (T)kStallEps) ? stalled + 1 : 0;
         prev = m;
@@ -212,10 +233,11 @@ int launch(const T* X, int64_t ldx, int s, int64_t n_units, const T* A, int64_t 
   const size_t scale_bytes = (sizeof(T) * (size_t)(n_units > 0 ? n_units : 1) + 255) & ~(size_t)255;
   const size_t total = scale_bytes + 256;
   if (query) { *need = total; return L1F_OK; }
-  auto kern = adm_small_kernel<T, KM, RPL, L>;
+  auto kern = E ? adm_small_kernel<T, KM, RPL, L, true> : adm_small_kernel<T, KM, RPL, L, false>;
   const int s_pad = RPL * L;
   const size_t smem = sizeof(T) * (size_t)s_pad * (KM + 1);
-  static int blocks_per_sm = 0;
+  static int bps_cache[2] = {0, 0};
+  int& blocks_per_sm = bps_cache[E ? 1 : 0];
   if (!blocks_per_sm) {
     L1F_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // the largest shared-memory carveout: the SMs keep room for a reconstruction CTA beside the
@@ -286,6 +308,8 @@ int l1f_small_dispatch(const T* X, int64_t ldx, int s, int64_t n_units, const T*
     if (s <= 128) L1F_SMALL(8, 8, 16);
     if (s <= 256) L1F_SMALL(8, 8, 32);
   } else if (k <= 10) {  // configs 1 and 4 (k = 10, s = 100): exact width, 8-lane groups
+    // 8 lanes x 13 rows for s <= 104 (the configs' s = 100; tools/r2/small_k_ab.py: cfg4 1.10 ms vs
+    // 1.23 ms for 16 x 7, 1.60 ms for 32 x 4); L1F_OPT_SMALL_LANES = 16 / 32 selects the others (A/B)
     const int64_t lanes = l1f::option(L1F_OPT_SMALL_LANES);
     if (s <= 112 && lanes == 16) L1F_SMALL(10, 7, 16);
     if (s <= 128 && lanes == 32) L1F_SMALL(10, 4, 32);
