@@ -107,10 +107,14 @@ C_OPTIONS = {"filter_streaming": 1, "filter_tc": 2, "tc_groups": 3, "recon_tc": 
 PY_OPTIONS = {"filter_pair": True, "sharded_stream": None, "small_k_fp64": 16}
 
 
+_c_option_cache = {}  # last value set through this module (the library's options change only via set_option)
+
+
 def set_option(name, value):
     """Set one option (C_OPTIONS: in the library; PY_OPTIONS: in the engine)."""
     if name in C_OPTIONS:
         call("l1f_set_option", C_OPTIONS[name], int(value))
+        _c_option_cache[name] = int(value)
     elif name in PY_OPTIONS:
         PY_OPTIONS[name] = value
     else:
@@ -118,9 +122,12 @@ def set_option(name, value):
 
 
 def get_option(name):
+    if name in _c_option_cache:  # hot path (engine checks per step): no ctypes round trip
+        return _c_option_cache[name]
     if name in C_OPTIONS:
         v = ctypes.c_int64(0)
         call("l1f_get_option", C_OPTIONS[name], ctypes.addressof(v))
+        _c_option_cache[name] = int(v.value)
         return int(v.value)
     if name in PY_OPTIONS:
         return PY_OPTIONS[name]
