@@ -448,11 +448,28 @@ def run_bench(args, rank, world, clock_sampler=None):
     t1 = time.perf_counter() - t0
     del block
     stepper = CudaShardedStep(m_local, plan, adm, u, sig, v)
-    for _ in range(max(3, args.warmup)):
-        stepper.step(m_local)
-    torch.cuda.synchronize()
+    # eager warm-up steps with events around the filters (kernel times; queued behind a device spin
+    # so the events time GPU work), then the step with its statistics all-reduce captured in a
+    # CUDA graph (kernels and NCCL collectives) for the timed steps; eager if capture fails
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(max(3, args.warmup))]
+    for i in range(len(evs)):
+        torch.cuda._sleep(4_000_000)
+        l_local, s_local, stats, (itc, itr) = stepper.step(m_local, evs[i])
+        torch.cuda.synchronize()
+    evs = evs[1:]
     dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+
+    def one_step():
+        out = stepper.step(m_local)
+        dist.all_reduce(out[2], group=None)  # statistics (exchange 3); sum over ranks
+        return out
+
+    try:
+        graph = engine.CapturedCall(one_step)
+        step_form = "CUDA graph (kernels + NCCL collectives), replayed"
+    except Exception as exc:  # capture unsupported: eager steps
+        graph, step_form = None, f"eager ({type(exc).__name__} at capture)"
+    dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = clock_sampler(int(os.environ.get("LOCAL_RANK", "0"))) if clock_sampler else None
     if sampler:
@@ -460,8 +477,7 @@ def run_bench(args, rank, world, clock_sampler=None):
     torch.cuda.synchronize()
     start.record()
     for i in range(args.steps):
-        l_local, s_local, stats, (itc, itr) = stepper.step(m_local, evs[i])
-        dist.all_reduce(stats, group=None)  # statistics (exchange 3); sum over ranks
+        l_local, s_local, stats, (itc, itr) = graph.replay() if graph is not None else one_step()
     end.record()
     torch.cuda.synchronize()
     if sampler:
@@ -524,6 +540,7 @@ def run_bench(args, rank, world, clock_sampler=None):
                 "filter": {"units": int(stats_h[2]), "mean_iters": float(stats_h[3] / max(stats_h[2], 1)),
                            "max_iters_summed_over_ranks": int(stats_h[0]), "failed_units": int(stats_h[1])},
                 "gpu_launches": stepper.launches_per_step * args.steps * world,
+                "step_form": step_form,
                 "gpu_launches_per_rank": stepper.launches_per_step * args.steps,
                 "clocks": sampler.summary() if sampler else None,
                 "e2e": {"value": m * n / (float(te.item()) * 1e-3) / 1e6, "unit": "M entries/s",

@@ -623,6 +623,28 @@ def _sm_count():
     return int(v.value)
 
 
+class CapturedCall:
+    """fn() captured once into a CUDA graph (after eager warm-up on a side stream) and replayed;
+    used for the sharded multi-GPU step, whose NCCL collectives are captured with its kernels."""
+
+    def __init__(self, fn, warmup=2):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = fn()
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+
 class CapturedStep:
     """solve_step captured once into a CUDA graph and replayed: the same kernels on the same
     buffers with no host work per step (small configurations are otherwise launch-bound:
