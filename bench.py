@@ -139,7 +139,7 @@ def cpu_leg(cfgd, seed_np, steps, target_s, ref=None, kind=None, validate=True):
     if ref is None:
         ref, kind = bench_cpu.load_reference()
     wl = bench_cpu.Workload(cfgd, seed=seed_np, ref=ref)
-    probe = 128
+    probe = 256
     best, settings = bench_cpu.pick_threads(ref, wl, probe)
     t_probe = settings[best.label()]["t_est_s"]
     # size the per-step sample so one step takes about target_s of CPU time
@@ -188,7 +188,7 @@ def run_reference(args):
     t_seed = time.perf_counter() - t0
     need = 6 * m * n * 8  # M, L, S, completion and the gathers, float64
     if kind == "reference" and need < 0.6 * _host_ram_bytes():
-        best, settings = bench_cpu.pick_threads(ref, wl, 128)
+        best, settings = bench_cpu.pick_threads(ref, wl, 256)
         t0 = time.perf_counter()
         m_full = bench_cpu.host_matrix(wl)
         t_regen = time.perf_counter() - t0
@@ -464,7 +464,7 @@ def cpu_baseline_leg(cfgd, seed_np, mode):
     m, n = cfgd["m"], cfgd["n"]
     if mode == "full" and kind == "reference" and 6 * m * n * 8 < 0.6 * _host_ram_bytes():
         wl = bench_cpu.Workload(cfgd, seed=seed_np, ref=ref)
-        best, settings = bench_cpu.pick_threads(ref, wl, 128)
+        best, settings = bench_cpu.pick_threads(ref, wl, 256)
         m_full = bench_cpu.host_matrix(wl)
         times, detail = bench_cpu.full_measure(ref, wl, m_full, best, 4, 0)
         del m_full

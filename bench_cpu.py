@@ -192,9 +192,9 @@ def pick_threads(ref, wl, units_probe):
     cores = len(os.sched_getaffinity(0))
     settings = [Threads(1, 1), Threads(cores, cores), Threads(1, cores)]
     res = {}
-    for th in settings:
-        out = sample_step(ref, wl, units_probe, th, rng_seed=99)
-        res[th.label()] = {"t_est_s": out["t_est"], "units": out["units"]}
+    for th in settings:  # best of two probes: oversubscribed settings are noisy run to run
+        outs = [sample_step(ref, wl, units_probe, th, rng_seed=99 + rep) for rep in range(2)]
+        res[th.label()] = {"t_est_s": min(o["t_est"] for o in outs), "units": outs[0]["units"]}
     best = min(settings, key=lambda th: res[th.label()]["t_est_s"])
     return best, res
 
