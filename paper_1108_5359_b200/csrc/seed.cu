@@ -4,10 +4,11 @@
 //   spectral_norm_est. pcp_adm.py:69-87    (25-step power iteration from the all-ones vector)
 //   svd / svt_with_rank matcore.py:73-105  (thin SVD; singular value thresholding)
 //
-// Blocks with min(m, n) <= 256 (every seed up to rank 25, the reference's test sizes) never reach
+// Blocks whose Jacobi working set fits in shared memory (square up to 113 x 113: every seed up to
+// rank 11, configs 1 and 4, the reference's test sizes) never reach
 // this file's library path: l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 hand them to the one-CTA
 // Jacobi kernels of seed_small.cu (no cuSOLVER, no host round trip).  Larger blocks (the rank-50
-// to rank-200 seeds of configs 2, 3 and 5, the full-matrix ADM) use cuSOLVER here: syevd on the
+// to rank-200 seeds of configs 2, 3 and 5, ranks 12-25, the full-matrix ADM) use cuSOLVER here: syevd on the
 // Gram matrix inside the ALM loop, gesvd for the public full SVD; the fused shrink/residual/dual
 // kernels, the deterministic reductions and the rank-k SVT products around them are ours.  The seed
 // runs in FP64: its factors must pass the reference's orthonormality check

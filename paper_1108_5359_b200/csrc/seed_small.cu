@@ -2,8 +2,9 @@
 // loop of solve_pcp (pcp_adm.py:90-140) with a hand-written one-sided Jacobi SVD for the singular
 // value thresholding (matcore.py:73-105), and a second kernel factors the final seed L
 // (recover_seed, l1filter.py:90-113 -> matcore.svd).  No library call and no host round trip: the
-// host reads one status record after the loop.  Used when min(m, n) <= kSmallMaxDim (every
-// l1-filtering seed up to rank 25: configs 1 and 4, the reference's test and golden sizes).
+// host reads one status record after the loop.  Used when the Jacobi working set (X, V) fits in
+// shared memory (square blocks up to 113 x 113: every l1-filtering seed up to rank 11 — configs 1
+// and 4, the reference's test and golden sizes; see l1f_seed_small_applies).
 //
 // One ALM iteration (all in the CTA, data in global memory / L1 / L2):
 //   S = shrink((M - L) + Y/b, lam/b);  W = (M - S) + Y/b                  (pcp_adm.py:122-123)
@@ -390,10 +391,15 @@ XvLayout xv_layout(int64_t mt, int64_t nt) {
 }
 }  // namespace
 
-// Whether the small-block path applies (l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 use it when it does).
+// Whether the small-block path applies (l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 use it when it
+// does): the Jacobi working set X (mt x nt) and V (nt x nt) must fit in shared memory — with them in
+// global memory the dependent dot -> rotate chain of a round costs ~16 us (measured: a 200 x 200 seed
+// took 0.68 s against 0.16 s through the Gram / syevd path), so larger blocks go there.
 bool l1f_seed_small_applies(int64_t m, int64_t n) {
   const int64_t p = m < n ? m : n, q = m < n ? n : m;
-  return p >= 1 && p <= kSmallMaxDim && q <= (1 << 16) && p * q <= (1 << 22);
+  if (!(p >= 1 && p <= kSmallMaxDim && q <= (1 << 16) && p * q <= (1 << 22))) return false;
+  const size_t bytes = sizeof(double) * ((size_t)(q | 1) * p + (size_t)(p | 1) * p);
+  return bytes <= 200 * 1024;
 }
 
 static int g_last_sweeps = 0;  // diagnostics: Jacobi sweeps of the last small-block solve
