@@ -466,9 +466,15 @@ def run_bench(args, rank, world, clock_sampler=None):
 
     try:
         graph = engine.CapturedCall(one_step)
-        step_form = "CUDA graph (kernels + NCCL collectives), replayed"
+        step_form, ok = "CUDA graph (kernels + NCCL collectives), replayed", 1.0
     except Exception as exc:  # capture unsupported: eager steps
-        graph, step_form = None, f"eager ({type(exc).__name__} at capture)"
+        graph, step_form, ok = None, f"eager ({type(exc).__name__} at capture)", 0.0
+    # the choice must be the same on every rank (a replayed graph's collectives pair with the
+    # other ranks' graph collectives only)
+    flag = torch.tensor([ok], dtype=torch.float64, device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if flag.item() < 1.0 and graph is not None:
+        graph, step_form = None, "eager (capture failed on another rank)"
     dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = clock_sampler(int(os.environ.get("LOCAL_RANK", "0"))) if clock_sampler else None
