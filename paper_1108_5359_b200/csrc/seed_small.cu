@@ -91,11 +91,12 @@ __device__ __forceinline__ double group_sum(double v) {
 }
 
 template <int G>
-__device__ int jacobi_g(double* X, int ldx, double* V, int ldv, int mt, int nt, int* flag) {
+__device__ int jacobi_g(double* X, int ldx, double* V, int ldv, int mt, int nt, int* flag, double loose_below) {
   constexpr int NG = NT / G;
   const int gl = threadIdx.x % G, grp = threadIdx.x / G;
   const int N = nt + (nt & 1);
   const double tolj = 2.220446049250313e-16 * sqrt((double)mt);
+  const double tolj2 = tolj * tolj;
   for (int sweep = 1; sweep <= kMaxSweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
@@ -123,10 +124,20 @@ __device__ int jacobi_g(double* X, int ldx, double* V, int ldv, int mt, int nt, 
         a = group_sum<G>(a);
         b = group_sum<G>(b);
         c = group_sum<G>(c);
-        if (!live || !(a > 0.0) || !(b > 0.0) || !(fabs(c) > tolj * sqrt(a) * sqrt(b))) continue;
-        const double zeta = (b - a) / (2.0 * c);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
-        const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+        // |c| > tol * sqrt(a b), squared: no square roots on the test (every warp runs this math for
+        // its pairs, and the round is instruction-issue bound)
+        // deep-bulk pairs (both squared norms below loose_below = eta^2 / 4 in the ALM) only need
+        // cosines below 1e-8: then every singular value of the deep-bulk columns stays below
+        // sqrt(1/4 + nt * 1e-8) eta < eta, so the thresholded result is that of the other columns,
+        // which are orthogonalised to eps * sqrt(mt) against everything (strict for the SVD itself)
+        const double tol2 = (a < loose_below && b < loose_below) ? 1e-16 : tolj2;
+        if (!live || !(a > 0.0) || !(b > 0.0) || !(c * c > tol2 * a * b)) continue;
+        // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) with zeta = (b - a) / 2c, multiplied through by
+        // |2c|: one square root and one division; cs = 1 / sqrt(1 + t^2) by rsqrt
+        const double d = b - a;
+        const double c2 = 2.0 * c;
+        const double t = (d >= 0.0 ? c2 : -c2) / (fabs(d) + sqrt(fma(d, d, c2 * c2)));
+        const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
         for (int i = gl; i < mt; i += G) {
           const double u = xa[i], v = xb[i];
@@ -150,8 +161,9 @@ __device__ int jacobi_g(double* X, int ldx, double* V, int ldv, int mt, int nt, 
   return -1;
 }
 
-__device__ int jacobi(double* X, int ldx, double* V, int ldv, int mt, int nt, int* flag) {
-  return (nt + 1) / 2 > NW ? jacobi_g<16>(X, ldx, V, ldv, mt, nt, flag) : jacobi_g<32>(X, ldx, V, ldv, mt, nt, flag);
+__device__ int jacobi(double* X, int ldx, double* V, int ldv, int mt, int nt, int* flag, double loose_below) {
+  return (nt + 1) / 2 > NW ? jacobi_g<16>(X, ldx, V, ldv, mt, nt, flag, loose_below)
+                           : jacobi_g<32>(X, ldx, V, ldv, mt, nt, flag, loose_below);
 }
 
 // per-column sigma = ||x_c|| (one warp per column)
@@ -238,8 +250,11 @@ alm_small_kernel(const double* __restrict__ M, int64_t ldm, int m, int n, double
     beta = 1.25 / (sigma > DBL_MIN ? sigma : DBL_MIN);
   }
   const double bmax = beta_max > 0.0 ? beta_max : 1e7 * beta;
-  double* X = use_smem ? smem_xv : w.X;
-  double* V = use_smem ? smem_xv + (size_t)ldx * sh.nt : w.V;
+  // X, V in shared memory (l1f_seed_small_applies admits only blocks whose working set fits):
+  // pointers derived from the shared array, so the Jacobi loads and stores are LDS / STS
+  (void)use_smem;
+  double* X = smem_xv;
+  double* V = smem_xv + (size_t)ldx * sh.nt;
   // V = I (warm start for the first iteration)
   for (int e = tid; e < sh.nt * ldv; e += NT) V[e] = (e / ldv == e % ldv) ? 1.0 : 0.0;
   __syncthreads();
@@ -257,7 +272,7 @@ alm_small_kernel(const double* __restrict__ M, int64_t ldm, int m, int n, double
     __syncthreads();
     gemm_tv(w.W, sh, V, ldv, X, ldx);
     __syncthreads();
-    const int sw = jacobi(X, ldx, V, ldv, sh.mt, sh.nt, &flag);
+    const int sw = jacobi(X, ldx, V, ldv, sh.mt, sh.nt, &flag, 0.25 * eta * eta);
     if (sw < 0) {
       if (tid == 0) st->err = L1F_ERR_SVD;
       return;
@@ -323,8 +338,9 @@ svd_small_kernel(const double* __restrict__ A, int64_t lda, int m, int n, double
   sh.mt = sh.tr ? n : m;
   sh.nt = sh.tr ? m : n;
   const int tid = threadIdx.x;
-  double* X = use_smem ? smem_xv : Xg;
-  double* V = use_smem ? smem_xv + (size_t)ldx * sh.nt : Vg;
+  (void)use_smem; (void)Xg; (void)Vg;
+  double* X = smem_xv;
+  double* V = smem_xv + (size_t)ldx * sh.nt;
   for (int e = tid; e < sh.nt * ldv; e += NT) V[e] = (e / ldv == e % ldv) ? 1.0 : 0.0;
   // X = T (V = I) from A with its leading dimension
   for (int e = tid; e < sh.mt * sh.nt; e += NT) {
@@ -332,7 +348,7 @@ svd_small_kernel(const double* __restrict__ A, int64_t lda, int m, int n, double
     X[(int64_t)c * ldx + i] = sh.tr ? A[(int64_t)c * lda + i] : A[(int64_t)i * lda + c];
   }
   __syncthreads();
-  const int sw = jacobi(X, ldx, V, ldv, sh.mt, sh.nt, &flag);
+  const int sw = jacobi(X, ldx, V, ldv, sh.mt, sh.nt, &flag, 0.0);
   if (sw < 0) {
     if (tid == 0) st->err = L1F_ERR_SVD;
     return;
@@ -426,6 +442,11 @@ int l1f_pcp_small(const double* M, int64_t ldm, int64_t m, int64_t n, double lam
   d += 64;
   w.act = (int*)d;
   Status* sp = (Status*)(w.act + nt + (nt & 1));
+  if (!xl.use_smem) {
+    set_error("pcp (small): working set does not fit in shared memory");
+    cudaFreeAsync(buf, st);
+    return L1F_ERR_UNSUPPORTED;
+  }
   if (xl.use_smem)
     cudaFuncSetAttribute(alm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xl.smem);
   alm_small_kernel<<<1, NT, xl.smem, st>>>(M, ldm, (int)m, (int)n, lam, tol, beta0, rho, beta_max, max_iter, L, S, w,
@@ -468,6 +489,11 @@ int l1f_svd_small(const double* W, int64_t m, int64_t n, int64_t ldw, double* U,
   double* s_tmp = Vw + (int64_t)xl.ldv * nt;
   int* order = (int*)(s_tmp + nt + 16);
   Status* sp = (Status*)(order + nt + (nt & 1) + 2);
+  if (!xl.use_smem) {
+    set_error("svd (small): working set does not fit in shared memory");
+    cudaFreeAsync(buf, st);
+    return L1F_ERR_UNSUPPORTED;
+  }
   if (xl.use_smem)
     cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xl.smem);
   svd_small_kernel<<<1, NT, xl.smem, st>>>(W, ldw, (int)m, (int)n, U, sigma, V, X, Vw, s_tmp, order, xl.ldx, xl.ldv,
