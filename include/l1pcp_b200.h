@@ -65,6 +65,12 @@ extern "C" {
                                        with the separate calls (the Python layer does)               */
 #define L1F_OPT_SMALL_LANES 9       /* lanes per unit of the k <= 10 filter kernel: 0 auto (8 for s <= 104),
                                        16 or 32                                                          */
+#define L1F_OPT_SEED_EIG 10         /* eigensolver of the Gram matrix in the seed SVT / factorisation for
+                                       blocks the small-block kernel does not take: 1 cuSOLVER syevd
+                                       (default: faster today), 0 the hand-written solver of eig_sym.cu
+                                       (tridiagonalisation + bisection + inverse iteration; same
+                                       results to ~3e-15, 1.3-3x slower)                                  */
+#define L1F_OPT_EIG_GRID 11         /* blocks of the hand-written tridiagonalisation (0 = automatic)    */
 int l1f_set_option(int key, int64_t value);
 int l1f_get_option(int key, int64_t* value_host);
 

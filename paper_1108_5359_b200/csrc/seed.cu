@@ -29,6 +29,8 @@ int l1f_pcp_small(const double* M, int64_t ldm, int64_t m, int64_t n, double lam
                   cudaStream_t st);
 int l1f_svd_small(const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sigma, double* V,
                   cudaStream_t st);
+int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* lam, double* Z, int* k_host,
+                      cudaStream_t st);
 
 namespace l1f {
 namespace seed {
@@ -274,6 +276,46 @@ static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double et
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)n, &zero, g.d(), p);
   else        // W W^T = X^T X
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)n, &zero, g.d(), p);
+  if (option(L1F_OPT_SEED_EIG) == 0) {
+    // hand-written eigensolver (eig_sym.cu): only the eigenpairs with lambda > eta^2, descending
+    Buf z(st);
+    L1F_CUDA_TRY(z.alloc(sizeof(double) * (size_t)p * p));
+    int kk = 0;
+    int rc = l1f_eig_sym_above(g.d(), p, eta * eta, 0.0, ev.d(), z.d(), &kk, st);
+    if (rc) return rc;
+    std::vector<double> lam((size_t)(kk > 0 ? kk : 1));
+    if (kk > 0) L1F_CUDA_TRY(cudaMemcpyAsync(lam.data(), ev.p, sizeof(double) * (size_t)kk, cudaMemcpyDeviceToHost, st));
+    L1F_CUDA_TRY(cudaStreamSynchronize(st));
+    int k = 0;
+    std::vector<double> c;
+    for (int j = 0; j < kk; ++j) {
+      const double sg = lam[(size_t)j] > 0.0 ? std::sqrt(lam[(size_t)j]) : 0.0;
+      if (!(sg > 0.0) || !(sg - eta > 0.0)) break;
+      c.push_back(1.0 - eta / sg);
+      ++k;
+    }
+    *rank = k;
+    if (k == 0) {
+      L1F_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)m * n, st));
+      return L1F_OK;
+    }
+    L1F_CUDA_TRY(cbuf.alloc(sizeof(double) * (size_t)k));
+    L1F_CUDA_TRY(cudaMemcpyAsync(cbuf.p, c.data(), sizeof(double) * (size_t)k, cudaMemcpyHostToDevice, st));
+    L1F_CUDA_TRY(t.alloc(sizeof(double) * (size_t)k * q));
+    const double* Vk = z.d();  // column-major p x k, descending
+    if (right) {
+      cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)m, (int)n, &one, Vk, p, W, (int)n, &zero, t.d(), k);
+      scale_rows_cm_kernel<<<num_sms() * 4, 256, 0, st>>>(t.d(), k, m, k, cbuf.d());
+      cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, k, &one, Vk, p, t.d(), k, &zero, out, (int)n);
+    } else {
+      cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, k, (int)m, &one, W, (int)n, Vk, p, &zero, t.d(), (int)n);
+      scale_cols_cm_kernel<<<num_sms() * 4, 256, 0, st>>>(t.d(), n, k, n, cbuf.d());
+      cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)m, k, &one, t.d(), (int)n, Vk, p, &zero, out, (int)n);
+    }
+    L1F_CHECK_LAUNCH();
+    L1F_CUDA_TRY(cudaStreamSynchronize(st));  // keep the host vector alive until consumed
+    return L1F_OK;
+  }
   int lwork = 0;
   if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
                                   &lwork) != CUSOLVER_STATUS_SUCCESS) {
@@ -418,6 +460,23 @@ __global__ void sigma_from_eig_kernel(const double* __restrict__ lam, int p, dou
   }
 }
 
+// eigenpairs from l1f_eig_sym_above (Z column-major p x k, lam descending) as a row-major p x p
+// eigenvector matrix (columns >= k zero), sigma = sqrt(lam) (0 beyond k) and its reciprocal
+__global__ void eig_pack_kernel(const double* __restrict__ Z, const double* __restrict__ lam, int k, int p,
+                                double* __restrict__ out, double* __restrict__ sig, double* __restrict__ inv) {
+  const int64_t total = (int64_t)p * p;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / p, j = x - i * p;
+    out[x] = j < k ? Z[j * (int64_t)p + i] : 0.0;
+  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p; j += gridDim.x * blockDim.x) {
+    const double l = j < k ? lam[j] : 0.0;
+    const double sg = l > 0.0 ? sqrt(l) : 0.0;
+    sig[j] = sg;
+    inv[j] = sg > 0.0 ? 1.0 / sg : 0.0;
+  }
+}
+
 static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sig, double* V,
                     cudaStream_t st) {
   const bool right = n <= m;
@@ -431,6 +490,18 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
   // row-major W (m x n, ld ldw) == column-major X = W^T (n x m, ld ldw)
   if (right) cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)ldw, &zero, g.d(), p);
   else cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)ldw, &zero, g.d(), p);
+  const int blocks = num_sms() * 4;
+  if (option(L1F_OPT_SEED_EIG) == 0) {
+    // hand-written eigensolver: the triplets with sigma > 1e-7 sigma_max (every seed rank cut keeps
+    // sigma > rank_tol * sigma_max with rank_tol >= 1e-6); the rest are returned as sigma = 0
+    Buf z(st);
+    L1F_CUDA_TRY(z.alloc(sizeof(double) * (size_t)p * p));
+    int kk = 0;
+    int rc = l1f_eig_sym_above(g.d(), p, 0.0, 1e-14, ev.d(), z.d(), &kk, st);
+    if (rc) return rc;
+    eig_pack_kernel<<<blocks, 256, 0, st>>>(z.d(), ev.d(), kk, p, right ? V : U, sig, inv.d());
+    L1F_CHECK_LAUNCH();
+  } else {
   int lwork = 0;
   if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
                                   &lwork) != CUSOLVER_STATUS_SUCCESS) {
@@ -452,17 +523,16 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
     return L1F_ERR_SVD;
   }
   sigma_from_eig_kernel<<<(p + 255) / 256, 256, 0, st>>>(ev.d(), p, sig, inv.d());
-  const int blocks = num_sms() * 4;
+  eig_desc_rowmajor_kernel<<<blocks, 256, 0, st>>>(g.d(), p, right ? V : U);
+  }
   if (right) {
     // V (n x p row-major) = eigenvectors; U (m x p row-major) = W V diag(1/sigma):
     // column-major U^T (p x m) = V^T (col-major view of V) * W^T (col-major view of W)
-    eig_desc_rowmajor_kernel<<<blocks, 256, 0, st>>>(g.d(), p, V);
     cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, (int)m, (int)n, &one, V, p, W, (int)ldw, &zero, U, p);
     scale_cols_kernel<<<blocks, 256, 0, st>>>(U, m, p, p, inv.d());
   } else {
     // U (m x p row-major) = eigenvectors; V (n x p row-major) = W^T U diag(1/sigma):
     // column-major V^T (p x n) = U^T (col-major view of U) * W (transpose of the col-major view)
-    eig_desc_rowmajor_kernel<<<blocks, 256, 0, st>>>(g.d(), p, U);
     cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_T, p, (int)n, (int)m, &one, U, p, W, (int)ldw, &zero, V, p);
     scale_cols_kernel<<<blocks, 256, 0, st>>>(V, n, p, p, inv.d());
   }
