@@ -33,12 +33,18 @@ TOL = 1e-7
 
 def load_reference():
     """(module, kind): the staged reference package, or the oracle port."""
-    path = os.path.join(ROOT, "oracle", "_ref")
-    if os.path.isdir(os.path.join(path, "l1pcp")):
-        if path not in sys.path:
-            sys.path.insert(0, path)
-        import l1pcp
-        return l1pcp, "reference"
+    pkg = os.path.join(ROOT, "oracle", "_ref", "l1pcp")
+    if os.path.isfile(os.path.join(pkg, "__init__.py")):
+        # imported under its own name from its own path: the module name "l1pcp" may be aliased
+        # to the drop-in elsewhere in the process (tests/reference_suite)
+        if "l1pcp_reference" not in sys.modules:
+            import importlib.util
+            spec = importlib.util.spec_from_file_location("l1pcp_reference", os.path.join(pkg, "__init__.py"),
+                                                          submodule_search_locations=[pkg])
+            mod = importlib.util.module_from_spec(spec)
+            sys.modules["l1pcp_reference"] = mod
+            spec.loader.exec_module(mod)
+        return sys.modules["l1pcp_reference"], "reference"
     return _PortShim(), "port"
 
 
