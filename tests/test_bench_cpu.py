@@ -54,3 +54,22 @@ def test_sampled_mode_and_extrapolation_check(ref):
                              f"blas=1,parallelism={len(os.sched_getaffinity(0))}"}
     chk = bench_cpu.validate_extrapolation(ref, "reference", TINY, 64, best)
     assert chk["full_s"] > 0 and np.isfinite(chk["rel_err"])
+
+
+def test_reference_arm_json_contract():
+    """`bench.py --impl reference` (the driver's reference arm) on config 1: one JSON line with the
+    contract's keys, timed on the staged reference package (kind "reference")."""
+    import json
+    import subprocess
+    if not os.path.isdir(os.path.join(ROOT, "oracle", "_ref", "l1pcp")):
+        pytest.skip("oracle/_ref not staged")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "config", "impl", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]

@@ -40,12 +40,12 @@ def test_host_pipeline_matches_device_solve(m, n, r, chunks):
     np.testing.assert_allclose(rs.cpu().numpy(), r_ref, rtol=1e-9, atol=1e-9 * r_ref[1])
 
 
-@pytest.mark.parametrize("pinned", [True, False])
-def test_public_api_host_tensor_path(pinned):
+@pytest.mark.parametrize("pinned,r", [(True, 25), (False, 25), (True, 8)])
+def test_public_api_host_tensor_path(pinned, r):
     """estimate_rank_and_solve on a float32 HOST tensor (the end-to-end call of bench.py's e2e):
     L, S come back as host tensors, bitwise equal to the device-resident public call; the seed
     block and the column panel are read zero-copy from host memory."""
-    m, n, r = 2500, 2200, 25
+    m, n = 2500, 2200  # r = 8: the FP64 small-k filter inside the pipeline
     mt, _, _, _ = engine.generate_matrix(m, n, r, 0.05, 500.0, seed=4)
     cfg = l1pcp.FilterConfig(rank_hint=r, rng_seed=0, adm=l1pcp.AdmConfig(tol=1e-7))
     dev = l1pcp.estimate_rank_and_solve(mt, cfg)
