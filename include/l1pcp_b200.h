@@ -70,7 +70,6 @@ extern "C" {
                                        (default: faster today), 0 the hand-written solver of eig_sym.cu
                                        (tridiagonalisation + bisection + inverse iteration; same
                                        results to ~3e-15, 1.3-3x slower)                                  */
-#define L1F_OPT_EIG_GRID 11         /* blocks of the hand-written tridiagonalisation (0 = automatic)    */
 int l1f_set_option(int key, int64_t value);
 int l1f_get_option(int key, int64_t* value_host);
 

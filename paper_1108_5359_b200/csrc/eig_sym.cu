@@ -41,88 +41,119 @@ __device__ double block_sum_det(double v, double* red) {
 
 // A: p x p row-major, full symmetric (overwritten).  Outputs d[p], e[p-1], tau[p-1], Vh[p][p]
 // (row i: v_i for columns i+1 .. p-1, v_i[i+1] = 1).  pv: p scratch, part: gridDim.x scratch.
-// Dynamic shared memory: v and w of the current step (2 p doubles), so the trailing-matrix streams
-// are the only global loads; rows are unrolled 4-deep to keep loads in flight.
+// Row r of the trailing block belongs to block r mod gridDim.x; the block's 8 warps split its rows'
+// columns into 8 contiguous chunks, so every warp has a few independent loads per lane per phase
+// (one L2 round trip) and the row sums of A v reduce in shared memory in a fixed order.  Dynamic
+// shared memory: v, w (2 p doubles) and the per-row warp partials.  Two grid barriers per column.
 __global__ void __launch_bounds__(TT) tridiag_kernel(double* __restrict__ A, int p, double* __restrict__ d,
                                                    double* __restrict__ e, double* __restrict__ tau_out,
                                                    double* __restrict__ Vh, double* __restrict__ pv,
                                                    double* __restrict__ part) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double sv[];  // v: [0, p), w: [p, 2p)
+  extern __shared__ double sv[];  // v: [0, p), w: [p, 2p), warp partials: [2p, 2p + 8 * rows_max)
   double* sw = sv + p;
+  double* wp = sv + 2 * p;
   __shared__ double red[TW + 1];
-  const int lane = threadIdx.x % 32;
-  const int gwarp = blockIdx.x * TW + threadIdx.x / 32, nwarps = gridDim.x * TW;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int G = gridDim.x, b = blockIdx.x;
   for (int i = 0; i + 1 < p; ++i) {
+    const int c0 = i + 1, len = p - c0;
     const double* rowi = A + (size_t)i * p;
+    // row i's tail into shared memory and its norm (every block; the reflector is recomputed
+    // identically everywhere)
     double s = 0.0;
-    for (int c = i + 2 + threadIdx.x; c < p; c += TT) s = fma(rowi[c], rowi[c], s);
+    for (int c = c0 + threadIdx.x; c < p; c += TT) {
+      const double x = rowi[c];
+      sv[c] = x;
+      if (c > c0) s = fma(x, x, s);
+    }
     const double xnorm2 = block_sum_det(s, red);
-    const double alpha = rowi[i + 1];
+    const double alpha = sv[c0];
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (xnorm2 > 0.0) {
       beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
       tau = (beta - alpha) / beta;
       scale = 1.0 / (alpha - beta);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (b == 0 && threadIdx.x == 0) {
       d[i] = rowi[i];
       e[i] = beta;
       tau_out[i] = tau;
     }
     if (tau == 0.0) {  // H = I: nothing to update (uniform across the grid)
-      for (int c = i + 1 + blockIdx.x * TT + threadIdx.x; c < p; c += gridDim.x * TT)
-        Vh[(size_t)i * p + c] = c == i + 1 ? 1.0 : 0.0;
+      for (int r = c0 + b * TT + threadIdx.x; r < p; r += G * TT) Vh[(size_t)i * p + r] = r == c0 ? 1.0 : 0.0;
+      __syncthreads();
       continue;
     }
-    for (int c = i + 1 + threadIdx.x; c < p; c += TT) sv[c] = c == i + 1 ? 1.0 : rowi[c] * scale;
+    for (int c = c0 + threadIdx.x; c < p; c += TT) sv[c] = c == c0 ? 1.0 : sv[c] * scale;
     __syncthreads();
-    // p_r = tau * sum_c A[r][c] v[c]  (rows r = i+1 .. p-1, one warp per row), partial p.v
-    double dot = 0.0;
-    const int c0 = i + 1;
-    for (int r = c0 + gwarp; r < p; r += nwarps) {
-      const double* ar = A + (size_t)r * p;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int c = c0 + lane;
-      for (; c + 96 < p; c += 128) {
-        a0 = fma(ar[c], sv[c], a0);
-        a1 = fma(ar[c + 32], sv[c + 32], a1);
-        a2 = fma(ar[c + 64], sv[c + 64], a2);
-        a3 = fma(ar[c + 96], sv[c + 96], a3);
+    // this block's rows r = first, first + G, ...; warp w takes columns [c0 + w*cl, c0 + (w+1)*cl)
+    const int first = c0 + ((b - c0 % G) + G) % G;
+    const int nrows = first < p ? (p - 1 - first) / G + 1 : 0;
+    const int cl = (len + TW - 1) / TW;
+    const int ca = c0 + warp * cl, cb = min(p, ca + cl);
+    // rows in groups of 8 with independent accumulators: 8 loads in flight per column step
+    for (int q0 = 0; q0 < nrows; q0 += 8) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = 0.0;
+      const double* ar = A + (size_t)(first + q0 * G) * p;
+      const size_t rstride = (size_t)G * p;
+      const int nu = min(8, nrows - q0);
+      for (int c = ca + lane; c < cb; c += 32) {
+        const double vc = sv[c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < nu) a[u] = fma(ar[u * rstride + c], vc, a[u]);
       }
-      for (; c < p; c += 32) a0 = fma(ar[c], sv[c], a0);
-      double a = warp_sum((a0 + a1) + (a2 + a3)) * tau;
-      if (lane == 0) {
-        pv[r] = a;
-        Vh[(size_t)i * p + r] = sv[r];
-        dot = fma(a, sv[r], dot);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double t = warp_sum(a[u]);
+        if (lane == 0 && u < nu) wp[(q0 + u) * TW + warp] = t;
       }
     }
+    __syncthreads();
+    double dot = 0.0;
+    for (int q = threadIdx.x; q < nrows; q += TT) {
+      const int r = first + q * G;
+      double a = 0.0;
+      for (int w = 0; w < TW; ++w) a += wp[q * TW + w];
+      a *= tau;
+      pv[r] = a;
+      Vh[(size_t)i * p + r] = sv[r];
+      dot = fma(a, sv[r], dot);
+    }
     dot = block_sum_det(dot, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = dot;
+    if (threadIdx.x == 0) part[b] = dot;
     grid.sync();
-    double pvdot = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) pvdot += part[b];
+    double ps = 0.0;
+    for (int x = threadIdx.x; x < G; x += TT) ps += part[x];
+    const double pvdot = block_sum_det(ps, red);
     const double K = -0.5 * tau * pvdot;
     for (int c = c0 + threadIdx.x; c < p; c += TT) sw[c] = fma(K, sv[c], pv[c]);
     __syncthreads();
-    // A[r][c] -= v[r] w[c] + w[r] v[c],  w = p + K v   (trailing block rows/cols i+1 .. p-1)
-    for (int r = c0 + gwarp; r < p; r += nwarps) {
-      double* ar = A + (size_t)r * p;
-      const double vr = sv[r], wr = sw[r];
-      int c = c0 + lane;
-      for (; c + 96 < p; c += 128) {
-        const double x0 = ar[c], x1 = ar[c + 32], x2 = ar[c + 64], x3 = ar[c + 96];
-        ar[c] = x0 - fma(vr, sw[c], wr * sv[c]);
-        ar[c + 32] = x1 - fma(vr, sw[c + 32], wr * sv[c + 32]);
-        ar[c + 64] = x2 - fma(vr, sw[c + 64], wr * sv[c + 64]);
-        ar[c + 96] = x3 - fma(vr, sw[c + 96], wr * sv[c + 96]);
+    // A[r][c] -= v[r] w[c] + w[r] v[c]  for this block's rows, warp w on its column chunk
+    for (int q0 = 0; q0 < nrows; q0 += 8) {
+      const int nu = min(8, nrows - q0);
+      double vr[8], wr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = first + (q0 + (u < nu ? u : 0)) * G;
+        vr[u] = sv[r];
+        wr[u] = sw[r];
       }
-      for (; c < p; c += 32) ar[c] -= fma(vr, sw[c], wr * sv[c]);
+      double* ar = A + (size_t)(first + q0 * G) * p;
+      const size_t rstride = (size_t)G * p;
+      for (int c = ca + lane; c < cb; c += 32) {
+        const double vc = sv[c], wc = sw[c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < nu) ar[u * rstride + c] -= fma(vr[u], wc, wr[u] * vc);
+      }
     }
     grid.sync();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) d[p - 1] = A[(size_t)(p - 1) * p + p - 1];
+  if (b == 0 && threadIdx.x == 0) d[p - 1] = A[(size_t)(p - 1) * p + p - 1];
 }
 
 // number of eigenvalues of T (d, e2 = e^2) below x
@@ -214,78 +245,92 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
 }
 
 // inverse iteration on T - s I (LU with partial pivoting, LAPACK dgttrf / dgttrs), two solves,
-// one thread per eigenvalue; Y column j (length p, contiguous) = the normalised vector
+// one thread per eigenvalue.  The per-eigenvalue factors live in scratch interleaved by eigenvalue
+// (entry i of eigenvalue j at [i * kp + j]) so a warp's loads and stores are coalesced; Y column j
+// (length p, contiguous) receives the normalised vector.
 __global__ void inverse_iter_kernel(const double* __restrict__ d, const double* __restrict__ e, int p, const Bounds* B,
-                                    const double* __restrict__ lam, double* __restrict__ Y, double* __restrict__ scratch) {
+                                    const double* __restrict__ lam, double* __restrict__ Y, double* __restrict__ scratch,
+                                    int kp) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= B->k) return;
   const double s = lam[j];
-  double* dl = scratch + (size_t)j * 5 * p;  // multipliers
-  double* dd = dl + p;                         // U diagonal
-  double* du = dd + p;                         // U first superdiagonal
-  double* du2 = du + p;                        // U second superdiagonal
-  double* y = Y + (size_t)j * p;
-  // factor (T - sI) = L U with partial pivoting (dgttrf); the row-interchange flags are kept in y
-  // (overwritten by the solution at the end), the right-hand side in the fifth scratch vector
+  const size_t plane = (size_t)p * kp;
+  double* dl = scratch + j;            // multipliers
+  double* dd = dl + plane;             // U diagonal
+  double* du = dd + plane;             // U first superdiagonal
+  double* du2 = du + plane;            // U second superdiagonal
+  double* bb = du2 + plane;            // right-hand side / solution
+  double* swp = bb + plane;            // row-interchange flags
+  auto at = [kp](double* a, int i) -> double& { return a[(size_t)i * kp]; };
   const double eps = 2.220446049250313e-16;
   const double tnorm = fmax(fabs(B->hi), fabs(B->lo)) + 1.0e-300;
-  for (int i = 0; i < p; ++i) {
-    dd[i] = d[i] - s;
-    du[i] = i + 1 < p ? e[i] : 0.0;
-    du2[i] = 0.0;
-  }
+  // factor (T - sI) = L U with partial pivoting (dgttrf), carrying the current diagonal and
+  // superdiagonal in registers
+  double di = d[0] - s, ui = p > 1 ? e[0] : 0.0;
   for (int i = 0; i + 1 < p; ++i) {
-    const double sub = e[i];  // subdiagonal (row i+1, col i)
-    if (fabs(dd[i]) >= fabs(sub)) {
-      const double f = dd[i] != 0.0 ? sub / dd[i] : 0.0;
-      dl[i] = f;
-      dd[i + 1] -= f * du[i];
-      y[i] = 0.0;  // no interchange
+    const double sub = e[i];
+    const double dn = d[i + 1] - s;
+    const double un = i + 2 < p ? e[i + 1] : 0.0;
+    if (fabs(di) >= fabs(sub)) {
+      const double f = di != 0.0 ? sub / di : 0.0;
+      at(dl, i) = f;
+      at(dd, i) = di;
+      at(du, i) = ui;
+      at(du2, i) = 0.0;
+      at(swp, i) = 0.0;
+      di = dn - f * ui;
+      ui = un;
     } else {
-      const double f = dd[i] / sub;
-      dd[i] = sub;
-      dl[i] = f;
-      const double t = du[i];
-      du[i] = dd[i + 1];
-      dd[i + 1] = t - f * dd[i + 1];
-      if (i + 2 < p) {
-        du2[i] = du[i + 1];
-        du[i + 1] = -f * du[i + 1];
-      }
-      y[i] = 1.0;  // interchange
+      const double f = di / sub;
+      at(dl, i) = f;
+      at(dd, i) = sub;
+      at(du, i) = dn;
+      at(du2, i) = un;
+      at(swp, i) = 1.0;
+      di = ui - f * dn;
+      ui = -f * un;
     }
   }
-  for (int i = 0; i < p; ++i)
-    if (fabs(dd[i]) < eps * tnorm) dd[i] = copysign(eps * tnorm, dd[i] == 0.0 ? 1.0 : dd[i]);
-  // right-hand side: a fixed, deterministic vector
-  double* b = du2 + p;
-  for (int i = 0; i < p; ++i) b[i] = 1.0 + 0.5 * sin(0.7 * (double)i + 0.3 * (double)j);
+  at(dd, p - 1) = di;
+  for (int i = 0; i < p; ++i) {
+    double& x = at(dd, i);
+    if (fabs(x) < eps * tnorm) x = copysign(eps * tnorm, x == 0.0 ? 1.0 : x);
+  }
+  for (int i = 0; i < p; ++i) at(bb, i) = 1.0 + 0.5 * sin(0.7 * (double)i + 0.3 * (double)j);
   for (int rep = 0; rep < 2; ++rep) {
-    // forward: apply L (with interchanges)
-    for (int i = 0; i + 1 < p; ++i) {
-      if (y[i] == 0.0) {
-        b[i + 1] -= dl[i] * b[i];
+    double prev = at(bb, 0);
+    for (int i = 0; i + 1 < p; ++i) {  // forward: L with the interchanges
+      const double nx = at(bb, i + 1);
+      if (at(swp, i) == 0.0) {
+        at(bb, i) = prev;
+        prev = nx - at(dl, i) * prev;
       } else {
-        const double t = b[i];
-        b[i] = b[i + 1];
-        b[i + 1] = t - dl[i] * b[i + 1];
+        at(bb, i) = nx;
+        prev = prev - at(dl, i) * nx;
       }
     }
-    // back substitution with U (diag dd, super du, du2)
-    double xn = b[p - 1] / dd[p - 1];
-    b[p - 1] = xn;
+    at(bb, p - 1) = prev;
+    double x1 = at(bb, p - 1) / at(dd, p - 1);  // back substitution with U
+    at(bb, p - 1) = x1;
+    double x2 = 0.0;
     if (p > 1) {
-      b[p - 2] = (b[p - 2] - du[p - 2] * b[p - 1]) / dd[p - 2];
+      x2 = x1;
+      x1 = (at(bb, p - 2) - at(du, p - 2) * x2) / at(dd, p - 2);
+      at(bb, p - 2) = x1;
     }
-    for (int i = p - 3; i >= 0; --i) b[i] = (b[i] - du[i] * b[i + 1] - du2[i] * b[i + 2]) / dd[i];
-    // normalise (and scale to avoid overflow in the next solve)
+    for (int i = p - 3; i >= 0; --i) {
+      const double x0 = (at(bb, i) - at(du, i) * x1 - at(du2, i) * x2) / at(dd, i);
+      at(bb, i) = x0;
+      x2 = x1;
+      x1 = x0;
+    }
     double nrm = 0.0;
-    for (int i = 0; i < p; ++i) nrm = fma(b[i], b[i], nrm);
-    nrm = sqrt(nrm);
-    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-    for (int i = 0; i < p; ++i) b[i] *= inv;
+    for (int i = 0; i < p; ++i) nrm = fma(at(bb, i), at(bb, i), nrm);
+    const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+    for (int i = 0; i < p; ++i) at(bb, i) *= inv;
   }
-  for (int i = 0; i < p; ++i) y[i] = b[i];
+  double* y = Y + (size_t)j * p;
+  for (int i = 0; i < p; ++i) y[i] = at(bb, i);
 }
 
 // classical Gram-Schmidt, twice (CGS2), over Y's k columns in descending eigenvalue order: nearly
@@ -298,10 +343,15 @@ __global__ void cgs2_kernel(double* __restrict__ Y, int p, const Bounds* B, cons
   __shared__ double red[32];
   const int k = B->k;
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+  // clusters: consecutive eigenvalues closer than 1e-4 ||T||; outside a cluster inverse iteration
+  // alone leaves the vectors orthogonal to ~eps ||T|| / gap <= 1e-12
+  const double gap_tol = 1e-4 * fmax(fabs(B->hi), fabs(B->lo));
+  int cstart = 0;
   for (int j = 0; j < k; ++j) {
+    if (j > 0 && !(fabs(lam[j - 1] - lam[j]) < gap_tol)) cstart = j;
     double* yj = Y + (size_t)j * p;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int i = warp; i < j; i += nw) {
+    for (int pass = 0; pass < 2 && cstart < j; ++pass) {
+      for (int i = cstart + warp; i < j; i += nw) {
         const double* yi = Y + (size_t)i * p;
         double s = 0.0;
         for (int r = lane; r < p; r += 32) s = fma(yi[r], yj[r], s);
@@ -311,7 +361,7 @@ __global__ void cgs2_kernel(double* __restrict__ Y, int p, const Bounds* B, cons
       __syncthreads();
       for (int r = threadIdx.x; r < p; r += blockDim.x) {
         double v = yj[r];
-        for (int i = 0; i < j; ++i) v = fma(-sdot[i], Y[(size_t)i * p + r], v);
+        for (int i = cstart; i < j; ++i) v = fma(-sdot[i], Y[(size_t)i * p + r], v);
         yj[r] = v;
       }
       __syncthreads();
@@ -335,23 +385,28 @@ __global__ void cgs2_kernel(double* __restrict__ Y, int p, const Bounds* B, cons
   }
 }
 
-// Z column j = Q y_j, Q = H_0 H_1 ... H_{p-2}: apply H_{p-2} .. H_0 in turn; one warp per column
+// Z column j = Q y_j, Q = H_0 H_1 ... H_{p-2}: H_{p-2} .. H_0 applied in turn; one block per column,
+// the column in shared memory, v rows read from global (contiguous)
 __global__ void backtransform_kernel(const double* __restrict__ Vh, const double* __restrict__ tau, int p,
                                      const Bounds* B, double* __restrict__ Y) {
-  const int lane = threadIdx.x % 32;
-  const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  extern __shared__ double sy[];
+  __shared__ double red[32];
+  const int j = blockIdx.x;
   if (j >= B->k) return;
   double* y = Y + (size_t)j * p;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) sy[c] = y[c];
+  __syncthreads();
   for (int i = p - 2; i >= 0; --i) {
     const double t = tau[i];
     if (t == 0.0) continue;
     const double* v = Vh + (size_t)i * p;
     double s = 0.0;
-    for (int c = i + 1 + lane; c < p; c += 32) s = fma(v[c], y[c], s);
-    s = warp_sum(s) * t;
-    for (int c = i + 1 + lane; c < p; c += 32) y[c] = fma(-s, v[c], y[c]);
-    __syncwarp();
+    for (int c = i + 1 + threadIdx.x; c < p; c += blockDim.x) s = fma(v[c], sy[c], s);
+    s = block_sum_det(s, red) * t;
+    for (int c = i + 1 + threadIdx.x; c < p; c += blockDim.x) sy[c] = fma(-s, v[c], sy[c]);
+    __syncthreads();
   }
+  for (int c = threadIdx.x; c < p; c += blockDim.x) y[c] = sy[c];
 }
 
 __global__ void symmetrize_kernel(double* __restrict__ A, int p) {
@@ -388,12 +443,16 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
     return L1F_ERR_UNSUPPORTED;
   }
   int per_sm = 0;
-  const size_t tri_smem = sizeof(double) * 2 * (size_t)p;
+  const int grid_target = 2 * nsm;  // two blocks per SM: 16 warps
+  const int rows_max = (p + grid_target - 1) / grid_target + 1;
+  const size_t tri_smem = sizeof(double) * (2 * (size_t)p + (size_t)TW * rows_max + 8);
   L1F_CUDA_TRY(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tri_smem));
   L1F_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridiag_kernel, TT, tri_smem));
-  const int64_t want = option(L1F_OPT_EIG_GRID);  // A/B: blocks of the tridiagonalisation (0 = auto)
-  int grid = std::max(1, std::min(nsm * std::max(per_sm, 1), std::max(1, (p + TW - 1) / TW)));
-  if (want > 0) grid = (int)std::min<int64_t>(want, (int64_t)nsm * std::max(per_sm, 1));
+  const int grid = grid_target;  // the shared-memory row partials are sized for this grid
+  if (per_sm < 2) {
+    set_error("eig_sym_above: occupancy below two blocks per SM");
+    return L1F_ERR_UNSUPPORTED;
+  }
   void* buf = nullptr;
   const size_t n_d = (size_t)p;
   const size_t bytes = sizeof(double) * (6 * n_d + (size_t)p * p + (size_t)grid + 8 * n_d * (size_t)p / 8 + 64) +
@@ -430,13 +489,14 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
       *k_host = k;
       if (k > 0) {
         void* sc = nullptr;
-        err = cudaMallocAsync(&sc, sizeof(double) * (size_t)k * 5 * p, st);
+        const int kp = (k + 31) / 32 * 32;
+        err = cudaMallocAsync(&sc, sizeof(double) * (size_t)kp * 6 * p, st);
         if (err == cudaSuccess) {
           bisect_kernel<<<(k + 7) / 8, 256, 0, st>>>(d, e2, p, B, 8, lam);
-          inverse_iter_kernel<<<(k + 63) / 64, 64, 0, st>>>(d, e, p, B, lam, Z, (double*)sc);
+          inverse_iter_kernel<<<(k + 31) / 32, 32, 0, st>>>(d, e, p, B, lam, Z, (double*)sc, kp);
           cudaFuncSetAttribute(cgs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * k));
           cgs2_kernel<<<1, 1024, sizeof(double) * (size_t)k, st>>>(Z, p, B, d, e, lam);
-          backtransform_kernel<<<(k + 7) / 8, 256, 0, st>>>(Vh, tau, p, B, Z);
+          backtransform_kernel<<<k, 256, sizeof(double) * (size_t)p, st>>>(Vh, tau, p, B, Z);
           err = cudaGetLastError();
           cudaFreeAsync(sc, st);
         }

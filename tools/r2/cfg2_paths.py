@@ -1,0 +1,26 @@
+"""cfg2: paired filter grid (default) vs the streamed form (two filter launches, reconstruction beside
+the row filter), both as CUDA-graph replays."""
+import sys, torch
+sys.path.insert(0, '.')
+import paper_1108_5359_b200 as l1pcp
+from paper_1108_5359_b200 import engine
+from paper_1108_5359_b200.synth import BENCHMARK_CONFIGS
+c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cfg = BENCHMARK_CONFIGS[c]
+mt, _, _, _ = engine.generate_matrix(cfg["m"], cfg["n"], cfg["r"], cfg["rho_s"], cfg["magnitude"], seed=0, kind=cfg["kind"])
+fcfg = l1pcp.FilterConfig(rank_hint=cfg["r"], rng_seed=0, adm=l1pcp.AdmConfig(tol=1e-7))
+kind, seed, _, _ = engine.seed_stage(mt, fcfg)
+plan = engine.FilterPlan(cfg["m"], cfg["n"], seed, mt.dtype, fcfg.adm)
+l, s = torch.empty_like(mt), torch.empty_like(mt)
+old = engine._streamed_ok
+for name, force in (("default", None), ("streamed", True), ("separate", False)):
+    if force is not None:
+        engine._streamed_ok = (lambda p, t, f=force: f)
+    g = engine.CapturedStep(plan, mt, l, s)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20): g.replay()
+    b.record(); torch.cuda.synchronize()
+    print(f"cfg{c} {name}: {a.elapsed_time(b)/20:.3f} ms/step", flush=True)
+    engine._streamed_ok = old
+    del g

@@ -4,8 +4,8 @@ from paper_1108_5359_b200 import engine, _lib
 torch.manual_seed(0)
 for p, r in ((1000, 100), (2000, 200)):
     a = torch.randn(p, r, dtype=torch.float64, device="cuda") @ torch.randn(r, p, dtype=torch.float64, device="cuda")
-    for g in (0, 8, 16, 32, 64, 128):
-        with _lib.options(seed_eig=0, eig_grid=g):
+    for g in (0,):
+        with _lib.options(seed_eig=0):
             engine.svd_device(a, gram=True); torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(3): engine.svd_device(a, gram=True)
