@@ -307,13 +307,18 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
     ev_all = ev_all[1:]  # the first eager step carries one-time costs
     # the timed steps replay the step captured into a CUDA graph (engine.CapturedStep): the same
     # kernels on the same buffers without per-step host work
-    graph = engine.CapturedStep(plan, mt, l_out, s_out)
+    try:
+        graph = engine.CapturedStep(plan, mt, l_out, s_out)
+        step_form = "CUDA graph of engine.solve_step (engine.CapturedStep), replayed per timed step"
+    except Exception as exc:  # capture unavailable: eager steps (same kernels, host enqueue per step)
+        graph, step_form = None, f"eager engine.solve_step ({type(exc).__name__} at graph capture)"
+        torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record(stream)
         for i in range(args.steps):
-            f = graph.replay()
+            f = graph.replay() if graph is not None else step()[0]
         end.record(stream)
         torch.cuda.synchronize()
     rs = f["resid_sq"]
@@ -335,7 +340,7 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
         torch.cuda.synchronize()
         t_recon = ra.elapsed_time(rb) / reps
         del af_s, bf_s
-        f = graph.replay()  # L, S of the streamed path again (the recovery check reads l_out)
+        f = graph.replay() if graph is not None else step()[0]  # L, S again (the recovery check reads l_out)
         rs = f["resid_sq"]
         torch.cuda.synchronize()
     else:
@@ -446,7 +451,7 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
         "value_incl_seed": m * n / (ms * 1e-3 + t1) / 1e6,
         "recovery_rel_err": rel, "residual": float(np.sqrt(r2 / m2)) if m2 else 0.0,
         "gpu_launches": launches_per_step * args.steps,
-        "step_form": "CUDA graph of engine.solve_step (engine.CapturedStep), replayed per timed step",
+        "step_form": step_form,
         "clocks": clk.summary(),
         "cpu_baseline": cpu_line,
         "e2e": e2e_line,
