@@ -70,6 +70,9 @@ extern "C" {
                                        (default: faster today), 0 the hand-written solver of eig_sym.cu
                                        (tridiagonalisation + bisection + inverse iteration; same
                                        results to ~3e-15, 1.3-3x slower)                                  */
+#define L1F_OPT_SEED_SMALL_SVT 11   /* SVT inside the one-CTA small-block ALM kernel: 1 Gram matrix +
+                                       shared-memory Householder tridiagonalisation + bisection +
+                                       inverse iteration (default), 0 one-sided Jacobi on the block   */
 int l1f_set_option(int key, int64_t value);
 int l1f_get_option(int key, int64_t* value_host);
 
