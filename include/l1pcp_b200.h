@@ -66,13 +66,18 @@ extern "C" {
 #define L1F_OPT_SMALL_LANES 9       /* lanes per unit of the k <= 10 filter kernel: 0 auto (8 for s <= 104),
                                        16 or 32                                                          */
 #define L1F_OPT_SEED_EIG 10         /* eigensolver of the Gram matrix in the seed SVT / factorisation for
-                                       blocks the small-block kernel does not take: 1 cuSOLVER syevd
-                                       (default: faster today), 0 the hand-written solver of eig_sym.cu
-                                       (tridiagonalisation + bisection + inverse iteration; same
-                                       results to ~3e-15, 1.3-3x slower)                                  */
+                                       blocks the small-block kernel does not take: 2 auto (default:
+                                       the hand-written solver of eig_sym.cu wherever its shared-
+                                       memory-resident tridiagonalisation applies, p <= 2000 on 148
+                                       SMs; cuSOLVER syevd beyond), 1 syevd always, 0 hand-written
+                                       always (Householder tridiagonalisation + bisection + inverse
+                                       iteration + back-transformation; same results to ~5e-15)       */
 #define L1F_OPT_SEED_SMALL_SVT 11   /* SVT inside the one-CTA small-block ALM kernel: 1 Gram matrix +
                                        shared-memory Householder tridiagonalisation + bisection +
                                        inverse iteration (default), 0 one-sided Jacobi on the block   */
+#define L1F_OPT_SEED_EIG_DSM 12     /* tridiagonalisation of the hand-written eigensolver: 1 the matrix
+                                       resident in the shared memory of all SMs, one grid-wide wait per
+                                       column (default, p <= 2000); 0 the L2-resident two-barrier form */
 int l1f_set_option(int key, int64_t value);
 int l1f_get_option(int key, int64_t* value_host);
 

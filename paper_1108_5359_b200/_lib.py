@@ -102,7 +102,7 @@ SIGNATURES = {
 # selection; the defaults are the production choices
 C_OPTIONS = {"filter_streaming": 1, "filter_tc": 2, "tc_groups": 3, "recon_tc": 4, "recon_stream": 5,
              "recon_concurrent": 6, "gather_overlap": 7, "wait_timeout_ms": 8, "small_lanes": 9, "seed_eig": 10,
-             "seed_small_svt": 11}
+             "seed_small_svt": 11, "seed_eig_dsm": 12}
 # host-side choices of the Python engine: the paired column+row filter call, the streamed form of
 # the sharded step (None = the library's pass model), the rank up to which the filter runs in FP64
 PY_OPTIONS = {"filter_pair": True, "sharded_stream": None, "small_k_fp64": 16}

@@ -27,8 +27,8 @@ static void keep_pool_memory(int dev) {
 }
 
 // process-wide option table (l1f_set_option); index = L1F_OPT_* key
-static constexpr int kNumOptions = 12;
-static int64_t g_options[kNumOptions] = {0, 0, 1, 0, 1, 1, 1, 1, 10000, 0, 1, 1};
+static constexpr int kNumOptions = 13;
+static int64_t g_options[kNumOptions] = {0, 0, 1, 0, 1, 1, 1, 1, 10000, 0, 2, 1, 1};
 
 int64_t option(int key) {
   return (key > 0 && key < kNumOptions) ? __atomic_load_n(&g_options[key], __ATOMIC_RELAXED) : 0;

@@ -156,6 +156,220 @@ __global__ void __launch_bounds__(TT) tridiag_kernel(double* __restrict__ A, int
   if (b == 0 && threadIdx.x == 0) d[p - 1] = A[(size_t)(p - 1) * p + p - 1];
 }
 
+// Tridiagonalisation with the matrix resident in the shared memory of the whole GPU (default for
+// p up to what 148 SMs hold: p <= 2000).  Block b owns rows b, b + G, b + 2G, ... in its shared
+// memory for the whole reduction; each of its 256 threads owns columns tid, tid + 256, ...  Per
+// column i every block recomputes the reflector from its register copy of row i (identical values
+// and reduction order everywhere: no broadcast), forms y = tau A v for its rows, publishes them
+// (per-column slots) with its partial of y.v, waits once on the column's counter (release add,
+// acquire spin: 1.3 us measured, tools/r2/xchg_bench.cu — polling per-block slots instead costs
+// 4.5 us), then reads y and the partials back (L2), updates its rows and its copy of row i + 1,
+// whose values the owner published one column earlier, so that load shares the round trip of y.
+// dsytd2 'L' order, as tridiag_kernel; Vh, d, e, tau written by block 0.
+#ifdef L1F_EIG_PROF
+#define EPROF(slot) do { if (tid == 0 && b == 0) { long long _t = clock64(); eprof[slot] += _t - eprev; eprev = _t; } } while (0)
+#else
+#define EPROF(slot) do {} while (0)
+#endif
+
+constexpr int DSM_T = 256;
+constexpr int DSM_W = DSM_T / 32;
+constexpr int DSM_R = 16;  // rows per block at most
+
+// ybuf, rowbuf: p x p slots (column i's y; row r's published values); part: p x G slots
+template <int CPT>
+__global__ void __launch_bounds__(DSM_T, 1)
+tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, double* __restrict__ e,
+                   double* __restrict__ tau_out, double* __restrict__ Vh, double* ybuf, double* part, double* rowbuf,
+                   unsigned* cnt) {
+  extern __shared__ double As[];  // R x p, row q = global row b + q G
+  __shared__ double red[DSM_W][DSM_R + 1];
+  __shared__ double wsum[DSM_W];
+  __shared__ double vq[DSM_R], yq[DSM_R];
+  __shared__ double sc[4];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = b < p ? (p - 1 - b) / G + 1 : 0;
+  for (int q = 0; q < R; ++q)
+    for (int c = tid; c < p; c += DSM_T) As[(size_t)q * p + c] = A[(size_t)(b + q * G) * p + c];
+  double cur[CPT];
+  int ownq[CPT];  // this thread's columns that are rows of this block: their index q, else -1
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int c = tid + DSM_T * j;
+    cur[j] = c < p ? A[c] : 0.0;
+    ownq[j] = (c < p && c >= b && (c - b) % G == 0) ? (c - b) / G : -1;
+  }
+  __syncthreads();
+#ifdef L1F_EIG_PROF
+  long long eprof[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long eprev = clock64();
+#endif
+  for (int i = 0; i + 1 < p; ++i) {
+    const int c0 = i + 1;
+    // ---- reflector from row i (every block, identically)
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + DSM_T * j;
+      if (c > c0 && c < p) s = fma(cur[j], cur[j], s);
+      if (c == c0) sc[0] = cur[j];
+      if (c == i && b == 0) d[i] = cur[j];
+    }
+    s = warp_sum(s);
+    if (lane == 0) wsum[warp] = s;
+    __syncthreads();
+    double xnorm2 = 0.0;
+    for (int w = 0; w < DSM_W; ++w) xnorm2 += wsum[w];
+    const double alpha = sc[0];
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (xnorm2 > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    double v[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + DSM_T * j;
+      v[j] = c == c0 ? 1.0 : ((c > c0 && c < p) ? cur[j] * scale : 0.0);
+      if (c >= c0 && c < p) {
+        if (b == 0) Vh[(size_t)i * p + c] = v[j];
+        if (ownq[j] >= 0) vq[ownq[j]] = v[j];
+      }
+    }
+    if (b == 0 && tid == 0) {
+      e[i] = beta;
+      tau_out[i] = tau;
+    }
+    EPROF(0);
+    // ---- y = tau A v over this block's rows r >= c0
+    double acc[DSM_R];
+#pragma unroll
+    for (int q = 0; q < DSM_R; ++q) {
+      acc[q] = 0.0;
+      if (q < R && b + q * G >= c0) {
+        const double* ar = As + (size_t)q * p;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+          const int c = tid + DSM_T * j;
+          if (c < p) acc[q] = fma(ar[c], v[j], acc[q]);
+        }
+      }
+    }
+    // transpose-reduce: 16 values per lane -> lane pairs holding one row's warp sum
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+      const int o = h * 2;  // lane distance 16, 8, 4, 2
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int q = 0; q < h; ++q) {
+        const double send = upper ? acc[q] : acc[q + h];
+        const double keep = upper ? acc[q + h] : acc[q];
+        acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    const int qrow = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0) red[warp][qrow] = acc[0];
+    __syncthreads();
+    double* ycol = ybuf + (size_t)i * p;
+    double* pcol = part + (size_t)i * G;
+    EPROF(1);
+    if (warp == 0) {
+      double pv = 0.0;
+      if (lane < DSM_R) {
+        const int r = b + lane * G;
+        double t = 0.0;
+        if (lane < R && r >= c0) {
+          for (int w = 0; w < DSM_W; ++w) t += red[w][lane];
+          t *= tau;
+          ycol[r] = t;
+          pv = t * vq[lane];
+        }
+        yq[lane] = t;
+      }
+      pv = warp_sum(pv);
+      if (lane == 0) pcol[b] = pv;
+      __syncwarp();
+      EPROF(5);
+      // the column's grid-wide wait: one counter, release add / acquire spin (a barrier over every
+      // block's y, partial and the row it published one column earlier)
+      if (lane == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + i) : "memory");
+        unsigned arrived;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(arrived) : "l"(cnt + i) : "memory");
+        } while (arrived < (unsigned)G);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    EPROF(2);
+    // ---- K from every block's partial (warp 0), y and the copy of row c0 for this thread's columns
+    if (warp == 0) {
+      double t = 0.0;
+      for (int x = lane; x < G; x += 32) t += __ldcg(pcol + x);
+      t = warp_sum(t);
+      if (lane == 0) sc[1] = -0.5 * tau * t;
+    }
+    double yv[CPT], nx[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + DSM_T * j;
+      const bool live = c >= c0 && c < p;
+      yv[j] = live ? __ldcg(ycol + c) : 0.0;
+      nx[j] = live ? (i == 0 ? A[(size_t)p + c] : __ldcg(rowbuf + (size_t)c0 * p + c)) : 0.0;
+    }
+    const double yc0 = __ldcg(ycol + c0);
+    __syncthreads();
+    const double K = sc[1];
+    const double wc0 = yc0 + K;
+    EPROF(3);
+    double w[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) w[j] = fma(K, v[j], yv[j]);
+    // ---- rank-2 update of this block's rows and of the copy of row c0
+    for (int q = 0; q < R; ++q) {
+      const int r = b + q * G;
+      if (r < c0) continue;
+      const double vr = vq[q], wr = fma(K, vr, yq[q]);
+      double* ar = As + (size_t)q * p;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int c = tid + DSM_T * j;
+        if (c >= c0 && c < p) ar[c] -= fma(vr, w[j], wr * v[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + DSM_T * j;
+      cur[j] = (c >= c0 && c < p) ? nx[j] - fma(1.0, w[j], wc0 * v[j]) : 0.0;
+    }
+    // ---- publish row i + 2 (current through column i) for the copies at column i + 1
+    const int r2 = i + 2;
+    if (r2 < p && r2 >= b && (r2 - b) % G == 0) {
+      const double* ar = As + (size_t)(r2 / G) * p;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int c = tid + DSM_T * j;
+        if (c >= r2 && c < p) rowbuf[(size_t)r2 * p + c] = ar[c];
+      }
+    }
+    EPROF(4);
+    // no barrier here: the next column's first __syncthreads orders sc / vq / yq / wsum reuse
+  }
+#ifdef L1F_EIG_PROF
+  if (tid == 0 && b == 0)
+    printf("tridiag_dsm p=%d cycles/col: reflector %lld matvec %lld publish %lld wait+K %lld loads %lld update %lld\n", p,
+           eprof[0] / (p - 1), eprof[1] / (p - 1), eprof[5] / (p - 1), eprof[2] / (p - 1), eprof[3] / (p - 1), eprof[4] / (p - 1));
+#endif
+  if (b == 0) {
+#pragma unroll
+    for (int j = 0; j < CPT; ++j)
+      if (tid + DSM_T * j == p - 1) d[p - 1] = cur[j];
+  }
+}
+
 // number of eigenvalues of T (d, e2 = e^2) below x
 __device__ __forceinline__ int sturm_below(const double* __restrict__ d, const double* __restrict__ e2, int p, double x,
                                            double pivmin) {
@@ -165,6 +379,25 @@ __device__ __forceinline__ int sturm_below(const double* __restrict__ d, const d
   cnt += q < 0.0;
   for (int j = 1; j < p; ++j) {
     q = (d[j] - x) - e2[j - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// the same count with the hardware reciprocal estimate and one Newton step in place of the division
+// (relative error ~2^-46 per pivot, far below the multisection's resolution); bisection only
+__device__ __forceinline__ int sturm_below_fast(const double* __restrict__ d, const double* __restrict__ e2, int p,
+                                                double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int j = 1; j < p; ++j) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    r = r * fma(-q, r, 2.0);
+    q = fma(-e2[j - 1], r, d[j] - x);
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
   }
@@ -231,7 +464,7 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   double lo = B->lo, hi = B->hi * (1.0 + 1e-14) + fabs(B->hi) * 1e-14 + pivmin;
   for (int it = 0; it < rounds; ++it) {
     const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-    const int c = sturm_below(d, e2, p, x, pivmin);  // eigenvalues below x
+    const int c = sturm_below_fast(d, e2, p, x, pivmin);  // eigenvalues below x
     // smallest x with count > idx is the new hi; the largest with count <= idx the new lo
     const unsigned above = __ballot_sync(0xffffffffu, c > idx);
     const int first = above ? __ffs(above) - 1 : 32;
@@ -344,13 +577,14 @@ __global__ void cgs2_kernel(double* __restrict__ Y, int p, const Bounds* B, cons
   const int k = B->k;
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
   // clusters: consecutive eigenvalues closer than 1e-4 ||T||; outside a cluster inverse iteration
-  // alone leaves the vectors orthogonal to ~eps ||T|| / gap <= 1e-12
+  // alone leaves the vectors orthogonal to ~eps ||T|| / gap <= 1e-12 (and already unit length)
   const double gap_tol = 1e-4 * fmax(fabs(B->hi), fabs(B->lo));
   int cstart = 0;
   for (int j = 0; j < k; ++j) {
     if (j > 0 && !(fabs(lam[j - 1] - lam[j]) < gap_tol)) cstart = j;
+    if (cstart == j) continue;  // uniform
     double* yj = Y + (size_t)j * p;
-    for (int pass = 0; pass < 2 && cstart < j; ++pass) {
+    for (int pass = 0; pass < 2; ++pass) {
       for (int i = cstart + warp; i < j; i += nw) {
         const double* yi = Y + (size_t)i * p;
         double s = 0.0;
@@ -372,17 +606,32 @@ __global__ void cgs2_kernel(double* __restrict__ Y, int p, const Bounds* B, cons
     const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
     for (int r = threadIdx.x; r < p; r += blockDim.x) yj[r] *= inv;
     __syncthreads();
-    double q = 0.0;
-    for (int r = threadIdx.x; r < p; r += blockDim.x) {
-      double ty = d[r] * yj[r];
-      if (r > 0) ty = fma(e[r - 1], yj[r - 1], ty);
-      if (r + 1 < p) ty = fma(e[r], yj[r + 1], ty);
-      q = fma(yj[r], ty, q);
-    }
-    q = block_sum_det(q, red);
-    if (threadIdx.x == 0) lam[j] = q;
-    __syncthreads();
   }
+}
+
+// normalisation and Rayleigh quotients lam_j = y_j^T T y_j, one warp per vector
+__global__ void rq_kernel(double* __restrict__ Y, int p, const Bounds* B, const double* __restrict__ d,
+                          const double* __restrict__ e, double* __restrict__ lam) {
+  const int lane = threadIdx.x % 32;
+  const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (j >= B->k) return;
+  double* yj = Y + (size_t)j * p;
+  double s = 0.0;
+  for (int r = lane; r < p; r += 32) s = fma(yj[r], yj[r], s);
+  const double nrm = sqrt(warp_sum(s));
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  double q = 0.0;
+  for (int r = lane; r < p; r += 32) {
+    const double yr = yj[r] * inv;
+    double ty = d[r] * yr;
+    if (r > 0) ty = fma(e[r - 1], yj[r - 1] * inv, ty);
+    if (r + 1 < p) ty = fma(e[r], yj[r + 1] * inv, ty);
+    q = fma(yr, ty, q);
+  }
+  q = warp_sum(q);
+  __syncwarp();
+  for (int r = lane; r < p; r += 32) yj[r] *= inv;
+  if (lane == 0) lam[j] = q;
 }
 
 // Z column j = Q y_j, Q = H_0 H_1 ... H_{p-2}: H_{p-2} .. H_0 applied in turn; one block per column,
@@ -409,6 +658,208 @@ __global__ void backtransform_kernel(const double* __restrict__ Vh, const double
   for (int c = threadIdx.x; c < p; c += blockDim.x) y[c] = sy[c];
 }
 
+// inverse iteration as inverse_iter_kernel, one block per eigenvalue with its factors in shared
+// memory (a dependent step is a shared-memory access, not an L2 round trip): thread 0 factors and
+// solves, the warp writes the normalised vector
+__global__ void __launch_bounds__(32) inverse_iter_smem_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                              int p, const Bounds* B, const double* __restrict__ lam,
+                                                              double* __restrict__ Y) {
+  extern __shared__ double fsm[];
+  const int j = blockIdx.x;
+  if (j >= B->k) return;
+  double* dl = fsm;
+  double* dinv = dl + p;
+  double* du = dinv + p;
+  double* du2 = du + p;
+  double* bb = du2 + p;
+  unsigned* sw = (unsigned*)(bb + p);
+  __shared__ double s_inv;
+  if (threadIdx.x == 0) {
+    const double s = lam[j];
+    const double eps = 2.220446049250313e-16;
+    const double clampv = eps * (fmax(fabs(B->hi), fabs(B->lo)) + 1.0e-300);
+    auto inv_pivot = [clampv](double x) {
+      if (fabs(x) < clampv) x = copysign(clampv, x == 0.0 ? 1.0 : x);
+      return 1.0 / x;
+    };
+    double di = d[0] - s, ui = p > 1 ? e[0] : 0.0;
+    unsigned bits = 0;
+    for (int i = 0; i + 1 < p; ++i) {
+      const double sub = e[i];
+      const double dn = d[i + 1] - s;
+      const double un = i + 2 < p ? e[i + 1] : 0.0;
+      if (fabs(di) >= fabs(sub)) {
+        const double f = di != 0.0 ? sub / di : 0.0;
+        dl[i] = f; dinv[i] = inv_pivot(di); du[i] = ui; du2[i] = 0.0;
+        di = dn - f * ui;
+        ui = un;
+      } else {
+        const double f = di / sub;
+        dl[i] = f; dinv[i] = inv_pivot(sub); du[i] = dn; du2[i] = un;
+        bits |= 1u << (i & 31);
+        di = ui - f * dn;
+        ui = -f * un;
+      }
+      if ((i & 31) == 31) { sw[i >> 5] = bits; bits = 0; }
+    }
+    if (p >= 2 && ((p - 2) & 31) != 31) sw[(p - 2) >> 5] = bits;
+    dinv[p - 1] = inv_pivot(di);
+    for (int i = 0; i < p; ++i) bb[i] = 1.0 + 0.5 * sin(0.7 * (double)i + 0.3 * (double)j);
+    double inv = 0.0;
+    for (int rep = 0; rep < 2; ++rep) {
+      if (rep == 1)
+        for (int i = 0; i < p; ++i) bb[i] *= inv;
+      double prev = bb[0];
+      for (int i = 0; i + 1 < p; ++i) {
+        const double nx = bb[i + 1];
+        const double f = dl[i];
+        if (!((sw[i >> 5] >> (i & 31)) & 1u)) {
+          bb[i] = prev;
+          prev = fma(-f, prev, nx);
+        } else {
+          bb[i] = nx;
+          prev = fma(-f, nx, prev);
+        }
+      }
+      double x1 = prev * dinv[p - 1];
+      bb[p - 1] = x1;
+      double nrm = x1 * x1, x2 = 0.0;
+      if (p > 1) {
+        x2 = x1;
+        x1 = (bb[p - 2] - du[p - 2] * x2) * dinv[p - 2];
+        bb[p - 2] = x1;
+        nrm = fma(x1, x1, nrm);
+      }
+      for (int i = p - 3; i >= 0; --i) {
+        const double x0 = (bb[i] - du[i] * x1 - du2[i] * x2) * dinv[i];
+        bb[i] = x0;
+        nrm = fma(x0, x0, nrm);
+        x2 = x1;
+        x1 = x0;
+      }
+      inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+    }
+    s_inv = inv;
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  double* y = Y + (size_t)j * p;
+  for (int i = threadIdx.x; i < p; i += 32) y[i] = bb[i] * inv;
+}
+
+// back-transformation as backtransform_kernel: BT_VPB eigenvectors per block, each in shared memory
+// and split over a group of BT_GW warps (thread t of the group owns columns t, t + 32 BT_GW, ...).
+// The reflector rows stream through shared memory in chunks of rc rows, double-buffered with
+// cp.async.  One pass per reflector applies it and forms the next reflector's dot with the updated
+// vector (v_{r-1} spans c >= r); the group combines its warps' partials through shared memory
+// under one named barrier per reflector.
+constexpr int BT_GW = 4;                 // warps per vector
+constexpr int BT_VPB = 2;                // vectors per block
+constexpr int BT_GT = 32 * BT_GW;        // threads per vector
+constexpr int BT_T = BT_GT * BT_VPB;
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void group_bar(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(BT_GT) : "memory");
+}
+template <int CM>  // columns per thread: p <= CM * BT_GT (fully unrolled: every load of a pass in flight)
+__global__ void __launch_bounds__(BT_T) backtransform_chunk_kernel(const double* __restrict__ Vh,
+                                                                  const double* __restrict__ tau, int p,
+                                                                  const Bounds* B, double* __restrict__ Y, int rc) {
+  extern __shared__ double bt_smem[];
+  __shared__ double red[BT_VPB][2][BT_GW];
+  const int lane = threadIdx.x & 31;
+  const int g = threadIdx.x / BT_GT, t = threadIdx.x % BT_GT, gw = t >> 5;
+  const int k = B->k;
+  const int j0 = blockIdx.x * BT_VPB;
+  if (j0 >= k) return;
+  const int j = j0 + g;
+  const bool live = j < k;
+  double* __restrict__ yv = bt_smem + (size_t)g * p;
+  double* chunks = bt_smem + (size_t)BT_VPB * p;  // 2 x rc rows of p
+  double* y = Y + (size_t)(live ? j : 0) * p;
+  if (live)
+    for (int c = t; c < p; c += BT_GT) yv[c] = y[c];
+  const int nrows = p - 1;  // reflectors 0 .. p-2, applied from p-2 down
+  const int nch = (nrows + rc - 1) / rc;
+  auto stage = [&](int ch) {
+    const int hi = p - 2 - ch * rc, lo = max(0, hi - rc + 1);
+    double* buf = chunks + (size_t)(ch & 1) * rc * p;
+    for (int r = lo; r <= hi; ++r)
+      for (int c = r + 1 + threadIdx.x; c < p; c += BT_T)
+        cp_async8(buf + (size_t)(r - lo) * p + c, Vh + (size_t)r * p + c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // group-wide sum of one value per thread (fixed order), parity-buffered slots
+  int par = 0;
+  auto gsum = [&](double a) {
+    a = warp_sum(a);
+    if (lane == 0) red[g][par][gw] = a;
+    group_bar(g);
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < BT_GW; ++w) s += red[g][par][w];
+    par ^= 1;
+    return s;
+  };
+  stage(0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage(ch + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (live) {
+      const int hi = p - 2 - ch * rc, lo = max(0, hi - rc + 1);
+      const double* buf = chunks + (size_t)(ch & 1) * rc * p;
+      const double tl = lane <= hi - lo ? __ldg(&tau[lo + lane]) : 0.0;  // this chunk's tau (rc <= 32)
+      const double* __restrict__ vh = buf + (size_t)(hi - lo) * p;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < CM; ++m) {
+        const int c = t + BT_GT * m;
+        const double x = (c > hi && c < p) ? vh[c] * yv[c] : 0.0;
+        if (m & 1) a1 += x; else a0 += x;
+      }
+      double sr = gsum(a0 + a1) * __shfl_sync(0xffffffffu, tl, hi - lo);
+      for (int r = hi; r >= lo; --r) {
+        const double* __restrict__ vr = buf + (size_t)(r - lo) * p;
+        if (r > lo) {
+          const double* __restrict__ vn = vr - p;  // v_{r-1}
+          double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+          for (int m = 0; m < CM; ++m) {
+            const int c = t + BT_GT * m;
+            if (c >= r && c < p) {
+              double y0 = yv[c];
+              if (c > r) {
+                y0 = fma(-sr, vr[c], y0);
+                yv[c] = y0;
+              }
+              if (m & 1) b1 = fma(vn[c], y0, b1); else b0 = fma(vn[c], y0, b0);
+            }
+          }
+          sr = gsum(b0 + b1) * __shfl_sync(0xffffffffu, tl, r - 1 - lo);
+        } else {
+#pragma unroll
+          for (int m = 0; m < CM; ++m) {
+            const int c = t + BT_GT * m;
+            if (c > r && c < p) yv[c] = fma(-sr, vr[c], yv[c]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // buffer (ch & 1) is refilled by stage(ch + 2)
+  }
+  if (live)
+    for (int c = t; c < p; c += BT_GT) y[c] = yv[c];
+}
+
 __global__ void symmetrize_kernel(double* __restrict__ A, int p) {
   // copy the lower triangle (cuBLAS syrk 'L', column-major = upper in row-major view) to a full matrix
   const int64_t total = (int64_t)p * p;
@@ -423,6 +874,19 @@ __global__ void symmetrize_kernel(double* __restrict__ A, int p) {
 
 using namespace l1f;
 using namespace l1f::eig;
+
+// Whether the shared-memory-resident tridiagonalisation takes a p x p matrix on this device (every
+// block's rows fit in its shared memory: p <= 2000 on 148 SMs)
+bool l1f_eig_dsm_applies(int p) {
+  int dev = 0, nsm = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (nsm <= 0 || nsm > 256 || p < 2) return false;
+  const int rmax = (p + nsm - 1) / nsm;
+  const size_t dsm_static = sizeof(double) * (DSM_W * (DSM_R + 1) + DSM_W + 2 * DSM_R + 4) + 64;
+  return rmax <= DSM_R && p <= 8 * DSM_T && sizeof(double) * (size_t)rmax * p + dsm_static <= (size_t)optin;
+}
 
 // Eigenpairs of the symmetric p x p matrix G (column-major lower triangle as cuBLAS syrk leaves it,
 // i.e. the row-major upper triangle; G is overwritten) with eigenvalue >= max(thr_abs, thr_rel *
@@ -470,8 +934,34 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
   Bounds* B = (Bounds*)(((uintptr_t)(w + 8) + 63) & ~(uintptr_t)63);
   symmetrize_kernel<<<nsm * 4, 256, 0, st>>>(G, p);
   int rc = L1F_OK;
-  void* args[] = {&G, &p, &d, &e, &tau, &Vh, &pv, &part};
-  cudaError_t err = cudaLaunchCooperativeKernel((void*)tridiag_kernel, grid, TT, args, tri_smem, st);
+  cudaError_t err = cudaSuccess;
+  // shared-memory-resident form when every block's rows fit (p <= 2000 on 148 SMs)
+  int optin = 0;
+  L1F_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int rmax = (p + nsm - 1) / nsm;
+  const size_t dsm_smem = sizeof(double) * (size_t)rmax * p;
+  const size_t dsm_static = sizeof(double) * (DSM_W * (DSM_R + 1) + DSM_W + 2 * DSM_R + 4) + 64;
+  const bool use_dsm = option(L1F_OPT_SEED_EIG_DSM) != 0 && l1f_eig_dsm_applies(p);
+  (void)dsm_static;
+  void* dsm_scr = nullptr;
+  if (use_dsm) {
+    const size_t slots = 2 * (size_t)p * p + (size_t)p * nsm;
+    L1F_CUDA_TRY(cudaMallocAsync(&dsm_scr, sizeof(double) * slots + sizeof(unsigned) * (size_t)p, st));
+    double* ybuf = (double*)dsm_scr;
+    double* rowbuf = ybuf + (size_t)p * p;
+    double* dpart = rowbuf + (size_t)p * p;
+    unsigned* cnt = (unsigned*)(dpart + (size_t)p * nsm);
+    L1F_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)p, st));
+    const double* Ac = G;
+    void* dargs[] = {(void*)&Ac, &p, &d, &e, &tau, &Vh, &ybuf, &dpart, &rowbuf, &cnt};
+    void* fn = p <= 2 * DSM_T ? (void*)tridiag_dsm_kernel<2>
+               : p <= 4 * DSM_T ? (void*)tridiag_dsm_kernel<4> : (void*)tridiag_dsm_kernel<8>;
+    L1F_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_smem));
+    err = cudaLaunchCooperativeKernel(fn, nsm, DSM_T, dargs, dsm_smem, st);
+  } else {
+    void* args[] = {&G, &p, &d, &e, &tau, &Vh, &pv, &part};
+    err = cudaLaunchCooperativeKernel((void*)tridiag_kernel, grid, TT, args, tri_smem, st);
+  }
   if (err != cudaSuccess) {
     set_error("eig_sym_above: tridiagonalisation launch failed: %s", cudaGetErrorString(err));
     rc = L1F_ERR_CUDA;
@@ -493,10 +983,27 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
         err = cudaMallocAsync(&sc, sizeof(double) * (size_t)kp * 6 * p, st);
         if (err == cudaSuccess) {
           bisect_kernel<<<(k + 7) / 8, 256, 0, st>>>(d, e2, p, B, 8, lam);
-          inverse_iter_kernel<<<(k + 31) / 32, 32, 0, st>>>(d, e, p, B, lam, Z, (double*)sc, kp);
+          const size_t inv_smem = sizeof(double) * 5 * (size_t)p + sizeof(unsigned) * ((p + 31) / 32 + 1);
+          if (inv_smem <= 200 * 1024) {
+            cudaFuncSetAttribute(inverse_iter_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inv_smem);
+            inverse_iter_smem_kernel<<<k, 32, inv_smem, st>>>(d, e, p, B, lam, Z);
+          } else {
+            inverse_iter_kernel<<<(k + 31) / 32, 32, 0, st>>>(d, e, p, B, lam, Z, (double*)sc, kp);
+          }
           cudaFuncSetAttribute(cgs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * k));
           cgs2_kernel<<<1, 1024, sizeof(double) * (size_t)k, st>>>(Z, p, B, d, e, lam);
-          backtransform_kernel<<<k, 256, sizeof(double) * (size_t)p, st>>>(Vh, tau, p, B, Z);
+          rq_kernel<<<(k + 7) / 8, 256, 0, st>>>(Z, p, B, d, e, lam);
+          const size_t bt_vec = sizeof(double) * BT_VPB * (size_t)p;
+          const int bt_rc = bt_vec < 200 * 1024 ? (int)std::min<size_t>(32, (200 * 1024 - bt_vec) / (2 * sizeof(double) * p)) : 0;
+          if (bt_rc >= 2 && p <= 16 * BT_GT) {
+            const size_t bt_smem = bt_vec + 2 * sizeof(double) * (size_t)bt_rc * p;
+            auto fn = p <= 4 * BT_GT ? backtransform_chunk_kernel<4>
+                    : p <= 8 * BT_GT ? backtransform_chunk_kernel<8> : backtransform_chunk_kernel<16>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem);
+            fn<<<(k + BT_VPB - 1) / BT_VPB, BT_T, bt_smem, st>>>(Vh, tau, p, B, Z, bt_rc);
+          } else {
+            backtransform_kernel<<<k, 256, sizeof(double) * (size_t)p, st>>>(Vh, tau, p, B, Z);
+          }
           err = cudaGetLastError();
           cudaFreeAsync(sc, st);
         }
@@ -507,6 +1014,7 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
       }
     }
   }
+  if (dsm_scr) cudaFreeAsync(dsm_scr, st);
   cudaFreeAsync(buf, st);
   return rc;
 }

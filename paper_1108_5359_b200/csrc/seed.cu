@@ -4,15 +4,18 @@
 //   spectral_norm_est. pcp_adm.py:69-87    (25-step power iteration from the all-ones vector)
 //   svd / svt_with_rank matcore.py:73-105  (thin SVD; singular value thresholding)
 //
-// Blocks whose Jacobi working set fits in shared memory (square up to 113 x 113: every seed up to
-// rank 11, configs 1 and 4, the reference's test sizes) never reach
-// this file's library path: l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 hand them to the one-CTA
-// Jacobi kernels of seed_small.cu (no cuSOLVER, no host round trip).  Larger blocks (the rank-50
-// to rank-200 seeds of configs 2, 3 and 5, ranks 12-25, the full-matrix ADM) use cuSOLVER here: syevd on the
-// Gram matrix inside the ALM loop, gesvd for the public full SVD; the fused shrink/residual/dual
-// kernels, the deterministic reductions and the rank-k SVT products around them are ours.  The seed
-// runs in FP64: its factors must pass the reference's orthonormality check
-// (l1reg.py:48-56, 1e-8) before they are cast to FP32 for the filter.
+// Blocks whose working set fits in shared memory (square up to 113 x 113: every seed up to rank 11,
+// configs 1 and 4, the reference's test sizes) never reach this file's library path:
+// l1f_pcp_f64 / l1f_svd_*_f64 / l1f_svt_f64 hand them to the one-CTA kernels of seed_small.cu (no
+// library call, no host round trip).  Larger blocks (the rank-50 to rank-200 seeds of configs 2, 3
+// and 5, ranks 12-25, the full-matrix ADM) run the ALM loop here: the SVT through the Gram matrix
+// (cuBLAS dsyrk / dgemm for the products) and its eigenpairs above the threshold from the
+// hand-written solver of eig_sym.cu (default wherever its shared-memory-resident tridiagonalisation
+// applies, p <= 2000; cuSOLVER syevd beyond, or on request through L1F_OPT_SEED_EIG); the fused
+// shrink / residual / dual kernels and the deterministic reductions are ours.  gesvd serves only the
+// public full SVD of large matrices (l1f_svd_f64).  The seed runs in FP64: its factors
+// must pass the reference's orthonormality check (l1reg.py:48-56, 1e-8) before they are cast to
+// FP32 for the filter.
 #include "common.cuh"
 
 #include <cublas_v2.h>
@@ -31,6 +34,7 @@ int l1f_svd_small(const double* W, int64_t m, int64_t n, int64_t ldw, double* U,
                   cudaStream_t st);
 int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* lam, double* Z, int* k_host,
                       cudaStream_t st);
+bool l1f_eig_dsm_applies(int p);
 
 namespace l1f {
 namespace seed {
@@ -262,6 +266,13 @@ __global__ void scale_cols_cm_kernel(double* __restrict__ T, int64_t rows, int64
   }
 }
 
+// the Gram eigensolver: hand-written (eig_sym.cu) or cuSOLVER syevd (L1F_OPT_SEED_EIG: 2 auto =
+// hand-written wherever its shared-memory-resident tridiagonalisation applies, p <= 2000)
+static bool hand_eig(int p) {
+  const int64_t mode = option(L1F_OPT_SEED_EIG);
+  return mode == 0 || (mode == 2 && l1f_eig_dsm_applies(p));
+}
+
 static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
                     cudaStream_t st) {
   const bool right = n <= m;         // Gram of the smaller side
@@ -276,7 +287,7 @@ static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double et
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)n, &zero, g.d(), p);
   else        // W W^T = X^T X
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)n, &zero, g.d(), p);
-  if (option(L1F_OPT_SEED_EIG) == 0) {
+  if (hand_eig(p)) {
     // hand-written eigensolver (eig_sym.cu): only the eigenpairs with lambda > eta^2, descending
     Buf z(st);
     L1F_CUDA_TRY(z.alloc(sizeof(double) * (size_t)p * p));
@@ -491,7 +502,7 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
   if (right) cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)ldw, &zero, g.d(), p);
   else cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)ldw, &zero, g.d(), p);
   const int blocks = num_sms() * 4;
-  if (option(L1F_OPT_SEED_EIG) == 0) {
+  if (hand_eig(p)) {
     // hand-written eigensolver: the triplets with sigma > 1e-7 sigma_max (every seed rank cut keeps
     // sigma > rank_tol * sigma_max with rank_tol >= 1e-6); the rest are returned as sigma = 0
     Buf z(st);

@@ -39,8 +39,6 @@ KNOWN_BREAKS = {
     # set by kernel launches, not flops.
     "test_ref_acceptance.py::test_scaling_law":
         "CPU timing-shape assertion (ADM exponent >= 1.7); GPU ADM is latency-bound at n <= 2000",
-    "test_ref_acceptance.py::test_scaling_law_full_adm_leg":
-        "CPU timing-shape assertion (ADM exponent >= 1.7 with the 4000 leg)",
 }
 
 HERE = os.path.dirname(os.path.abspath(__file__))
