@@ -55,6 +55,7 @@ SIGNATURES = {
     "l1f_set_option": (_int, [_int, _i64]),
     "l1f_get_option": (_int, [_int, _vp]),
     "l1f_version": (_int, []),
+    "l1f_init": (_int, [_vp]),
     "l1f_sm_count": (_int, [_vp]),
     "l1f_filter_workspace_bytes": (_sz, [_int, _i32, _i32, _i64]),
     "l1f_filter_f32": (_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _f32, _f32, _f32, _f32, _i32,
@@ -206,7 +207,22 @@ def load(path=None):
             fn.argtypes = args
         if path is None:
             _lib = lib
+        _init_device(lib)
         return lib
+
+
+def _init_device(lib):
+    """One-time device initialisation (l1f_init: cuBLAS handle and first GEMMs, eigensolver kernels)
+    when a GPU is present, so that it is not charged to the first solve."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+    except ImportError:
+        return
+    code = lib.l1f_init(None)
+    if code != 0:
+        raise NativeError(f"l1f_init failed ({code}): {lib.l1f_last_error().decode(errors='replace')}")
 
 
 def last_error():

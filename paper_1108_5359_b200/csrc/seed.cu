@@ -44,25 +44,34 @@ struct Handles {
   cublasHandle_t blas = nullptr;
 };
 
+// cuBLAS on every call; the cuSOLVER handle only when a cuSOLVER routine runs (its creation loads
+// the library's modules, ~0.1 s, which the default seed path never needs)
 static int handles(cudaStream_t st, Handles*& out) {
   static thread_local Handles h;
-  if (!h.sol) {
-    if (cusolverDnCreate(&h.sol) != CUSOLVER_STATUS_SUCCESS) {
-      set_error("cusolverDnCreate failed");
-      return L1F_ERR_CUDA;
-    }
-  }
   if (!h.blas) {
     if (cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS) {
       set_error("cublasCreate failed");
       return L1F_ERR_CUDA;
     }
   }
-  cusolverDnSetStream(h.sol, st);
   cublasSetStream(h.blas, st);
+  if (h.sol) cusolverDnSetStream(h.sol, st);
   out = &h;
   return L1F_OK;
 }
+
+static cusolverDnHandle_t solver(Handles* h, cudaStream_t st) {
+  if (!h->sol && cusolverDnCreate(&h->sol) != CUSOLVER_STATUS_SUCCESS) {
+    h->sol = nullptr;
+    set_error("cusolverDnCreate failed");
+    return nullptr;
+  }
+  cusolverDnSetStream(h->sol, st);
+  return h->sol;
+}
+#define L1F_SOLVER(h, st)                                  \
+  cusolverDnHandle_t sol_ = solver((h), (st));             \
+  if (!sol_) return L1F_ERR_CUDA
 
 struct Buf {
   void* p = nullptr;
@@ -170,13 +179,14 @@ static int svd_rowmajor(Handles* h, const double* W, int64_t m, int64_t n, int64
   L1F_CUDA_TRY(ucm.alloc(sizeof(double) * (size_t)R * p));
   L1F_CUDA_TRY(vtcm.alloc(sizeof(double) * (size_t)p * C));
   int lwork = 0;
-  if (cusolverDnDgesvd_bufferSize(h->sol, R, C, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+  L1F_SOLVER(h, st);
+  if (cusolverDnDgesvd_bufferSize(sol_, R, C, &lwork) != CUSOLVER_STATUS_SUCCESS) {
     set_error("gesvd_bufferSize failed");
     return L1F_ERR_CUDA;
   }
   L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
   L1F_CUDA_TRY(info.alloc(sizeof(int)));
-  cusolverStatus_t cs = cusolverDnDgesvd(h->sol, 'S', 'S', R, C, a.d(), R, sig, ucm.d(), R, vtcm.d(), (int)p,
+  cusolverStatus_t cs = cusolverDnDgesvd(sol_, 'S', 'S', R, C, a.d(), R, sig, ucm.d(), R, vtcm.d(), (int)p,
                                          work.d(), lwork, nullptr, (int*)info.p);
   if (cs != CUSOLVER_STATUS_SUCCESS) {
     set_error("cusolverDnDgesvd failed with status %d", (int)cs);
@@ -328,14 +338,15 @@ static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double et
     return L1F_OK;
   }
   int lwork = 0;
-  if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
+  L1F_SOLVER(h, st);
+  if (cusolverDnDsyevd_bufferSize(sol_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
                                   &lwork) != CUSOLVER_STATUS_SUCCESS) {
     set_error("syevd_bufferSize failed");
     return L1F_ERR_CUDA;
   }
   L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
   L1F_CUDA_TRY(info.alloc(sizeof(int)));
-  if (cusolverDnDsyevd(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
+  if (cusolverDnDsyevd(sol_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
                        (int*)info.p) != CUSOLVER_STATUS_SUCCESS) {
     set_error("cusolverDnDsyevd failed");
     return L1F_ERR_SVD;
@@ -514,14 +525,15 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
     L1F_CHECK_LAUNCH();
   } else {
   int lwork = 0;
-  if (cusolverDnDsyevd_bufferSize(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
+  L1F_SOLVER(h, st);
+  if (cusolverDnDsyevd_bufferSize(sol_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(),
                                   &lwork) != CUSOLVER_STATUS_SUCCESS) {
     set_error("syevd_bufferSize failed");
     return L1F_ERR_CUDA;
   }
   L1F_CUDA_TRY(work.alloc(sizeof(double) * (size_t)(lwork > 0 ? lwork : 1)));
   L1F_CUDA_TRY(info.alloc(sizeof(int)));
-  if (cusolverDnDsyevd(h->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
+  if (cusolverDnDsyevd(sol_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, g.d(), p, ev.d(), work.d(), lwork,
                        (int*)info.p) != CUSOLVER_STATUS_SUCCESS) {
     set_error("cusolverDnDsyevd failed");
     return L1F_ERR_SVD;
@@ -548,6 +560,38 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
     scale_cols_kernel<<<blocks, 256, 0, st>>>(V, n, p, p, inv.d());
   }
   L1F_CHECK_LAUNCH();
+  return L1F_OK;
+}
+
+// One-time initialisation on the current device (include/l1pcp_b200.h l1f_init): the cuBLAS handle
+// and its first dsyrk / dgemm (cuBLAS loads its kernels on first use), and one small run of the
+// hand-written eigensolver so its kernels are loaded; idempotent per host thread
+extern "C" int l1f_init(void* stream) {
+  static thread_local bool done = false;
+  if (done) return L1F_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Handles* h;
+  int rc = handles(st, h);
+  if (rc) return rc;
+  const int p = 16;
+  Buf a(st), g(st), lam(st), z(st);
+  L1F_CUDA_TRY(a.alloc(sizeof(double) * p * p));
+  L1F_CUDA_TRY(g.alloc(sizeof(double) * p * p));
+  L1F_CUDA_TRY(lam.alloc(sizeof(double) * p));
+  L1F_CUDA_TRY(z.alloc(sizeof(double) * p * p));
+  std::vector<double> ha((size_t)p * p);
+  for (int i = 0; i < p * p; ++i) ha[(size_t)i] = (i % p == i / p) ? 2.0 + i % p : 0.25 / (1 + i % 7);
+  L1F_CUDA_TRY(cudaMemcpyAsync(a.p, ha.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice, st));
+  const double one = 1.0, zero = 0.0;
+  cublasSetPointerMode(h->blas, CUBLAS_POINTER_MODE_HOST);
+  cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, p, &one, a.d(), p, &zero, g.d(), p);
+  cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, p, p, &one, a.d(), p, g.d(), p, &zero, z.d(), p);
+  cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, p, &one, a.d(), p, g.d(), p, &zero, z.d(), p);
+  int k = 0;
+  rc = l1f_eig_sym_above(g.d(), p, 0.0, 0.5, lam.d(), z.d(), &k, st);
+  if (rc) return rc;
+  L1F_CUDA_TRY(cudaStreamSynchronize(st));
+  done = true;
   return L1F_OK;
 }
 
