@@ -1,7 +1,8 @@
-"""The hand-written symmetric eigensolver (csrc/eig_sym.cu: cooperative Householder
-tridiagonalisation, Sturm multisection, inverse iteration, CGS2, back-transformation) that replaces
-cuSOLVER syevd in the large-seed SVT when L1F_OPT_SEED_EIG = 0: same singular values, factors and
-seed solves as the syevd path (reference: the SVD inside svt_with_rank, matcore.py:73-105)."""
+"""The hand-written symmetric eigensolvers of the seed SVT (csrc/eig_sym.cu: cooperative Householder
+tridiagonalisation, Sturm multisection, inverse iteration, CGS2, back-transformation; csrc/seed_small.cu:
+the one-CTA Gram / shared-memory tridiagonal SVT): same singular values, factors and seed solves as the
+cuSOLVER syevd path (L1F_OPT_SEED_EIG = 1) and the one-sided Jacobi SVT (L1F_OPT_SEED_SMALL_SVT = 0)
+(reference: the SVD inside svt_with_rank, matcore.py:73-105)."""
 
 import numpy as np
 import pytest
@@ -43,3 +44,57 @@ def test_seed_stage_matches_syevd_path():
     assert k0 == k1 == "seed" and a0 == a1
     assert s0.r_prime == s1.r_prime == r and s0.pcp_iterations == s1.pcp_iterations
     assert float((s0.seed_l - s1.seed_l).norm() / s1.seed_l.norm()) <= 1e-12
+
+
+def _pcp_case(m, n, r, seed, rho=0.1):
+    rng = np.random.default_rng(seed)
+    low = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    sp = np.where(rng.random((m, n)) < rho, rng.uniform(-50, 50, (m, n)), 0.0)
+    return torch.from_numpy(low + sp).cuda()
+
+
+@pytest.mark.parametrize("m,n,r", [(130, 120, 6), (120, 300, 8), (400, 160, 12), (700, 600, 30)])
+@pytest.mark.parametrize("dsm", [1, 0])
+def test_large_block_pcp_matches_syevd(m, n, r, dsm):
+    """The ALM loop on blocks beyond the one-CTA kernel with the hand-written eigensolver (shared-
+    memory-resident or L2-resident tridiagonalisation; p = min(m, n) from 120, fewer rows than the
+    148 blocks, to 600) against the syevd path: same iterations and rank, L to 1e-12."""
+    from paper_1108_5359_b200 import pcp_adm
+    M = _pcp_case(m, n, r, m * 7 + n)
+    cfg = pcp_adm.AdmConfig(tol=1e-7)
+    with _lib.options(seed_eig=0, seed_eig_dsm=dsm):
+        l0, s0, i0 = pcp_adm.solve_pcp_device(M, cfg)
+    with _lib.options(seed_eig=1):
+        l1, s1, i1 = pcp_adm.solve_pcp_device(M, cfg)
+    assert i0["iterations"] == i1["iterations"] and i0["rank"] == i1["rank"]
+    assert float((l0 - l1).norm() / l1.norm()) <= 1e-12
+    assert float((s0 - s1).abs().max()) <= 1e-9 * float(M.abs().max())
+
+
+@pytest.mark.parametrize("m,n,r", [(7, 1, 1), (1, 9, 1), (5, 3, 1), (20, 20, 2), (113, 113, 11), (64, 200, 5),
+                                   (100, 40, 4)])
+def test_small_block_gram_svt_matches_jacobi(m, n, r):
+    """The one-CTA ALM kernel's Gram / shared-memory tridiagonal SVT (default) against its one-sided
+    Jacobi SVT on edge shapes (a single row or column, rectangular, the 113 x 113 limit): same
+    iterations and rank, L to 1e-8 relative."""
+    from paper_1108_5359_b200 import pcp_adm
+    M = _pcp_case(m, n, r, m * 11 + n)
+    cfg = pcp_adm.AdmConfig(tol=1e-7)
+    with _lib.options(seed_small_svt=1):
+        l0, s0, i0 = pcp_adm.solve_pcp_device(M, cfg)
+    with _lib.options(seed_small_svt=0):
+        l1, s1, i1 = pcp_adm.solve_pcp_device(M, cfg)
+    assert i0["iterations"] == i1["iterations"]
+    # a single row / column leaves L at roundoff (~1e-16), its one singular value at the threshold
+    roundoff = float(l1.norm()) <= 1e-12 * float(M.norm())
+    assert i0["rank"] == i1["rank"] or (roundoff and abs(i0["rank"] - i1["rank"]) <= 1)
+    # relative to L, or to M where L is roundoff
+    assert float((l0 - l1).norm()) <= 1e-8 * max(float(l1.norm()), 1e-6 * float(M.norm()))
+
+
+def test_small_block_zero_matrix():
+    from paper_1108_5359_b200 import pcp_adm
+    M = torch.zeros(50, 60, dtype=torch.float64, device="cuda")
+    l, s, info = pcp_adm.solve_pcp_device(M, pcp_adm.AdmConfig(tol=1e-7))
+    assert info["iterations"] == 1
+    assert float(l.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
