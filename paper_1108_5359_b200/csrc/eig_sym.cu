@@ -404,6 +404,31 @@ __device__ __forceinline__ int sturm_below_fast(const double* __restrict__ d, co
   return cnt;
 }
 
+// reciprocal from the hardware estimate and two Newton steps (within an ulp of 1 / x; off the
+// IEEE division's slow path, which dominates a dependent chain of p steps)
+__device__ __forceinline__ double rcp_nr2(double x) {
+  if (!(fabs(x) > 4.0 * DBL_MIN)) return 1.0 / x;  // the estimate flushes subnormals
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+
+// count of eigenvalues below x with rcp_nr2 pivots (the threshold count of bounds_kernel)
+__device__ __forceinline__ int sturm_below_nr2(const double* __restrict__ d, const double* __restrict__ e2, int p,
+                                               double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int j = 1; j < p; ++j) {
+    q = fma(-e2[j - 1], rcp_nr2(q), d[j] - x);
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
 struct Bounds {
   double lo, hi, pivmin;
   int k;
@@ -448,7 +473,7 @@ __global__ void bounds_kernel(const double* __restrict__ d, const double* __rest
     B->pivmin = pivmin;
     const double thr = fmax(thr_abs, thr_rel * fmax(fabs(shi), fabs(B->lo)));
     B->lo = thr;  // bracket from the threshold
-    B->k = p - sturm_below(d, e2, p, thr, pivmin);
+    B->k = p - sturm_below_nr2(d, e2, p, thr, pivmin);
   }
 }
 
@@ -680,7 +705,7 @@ __global__ void __launch_bounds__(32) inverse_iter_smem_kernel(const double* __r
     const double clampv = eps * (fmax(fabs(B->hi), fabs(B->lo)) + 1.0e-300);
     auto inv_pivot = [clampv](double x) {
       if (fabs(x) < clampv) x = copysign(clampv, x == 0.0 ? 1.0 : x);
-      return 1.0 / x;
+      return rcp_nr2(x);
     };
     double di = d[0] - s, ui = p > 1 ? e[0] : 0.0;
     unsigned bits = 0;
@@ -689,12 +714,12 @@ __global__ void __launch_bounds__(32) inverse_iter_smem_kernel(const double* __r
       const double dn = d[i + 1] - s;
       const double un = i + 2 < p ? e[i + 1] : 0.0;
       if (fabs(di) >= fabs(sub)) {
-        const double f = di != 0.0 ? sub / di : 0.0;
+        const double f = di != 0.0 ? sub * rcp_nr2(di) : 0.0;
         dl[i] = f; dinv[i] = inv_pivot(di); du[i] = ui; du2[i] = 0.0;
         di = dn - f * ui;
         ui = un;
       } else {
-        const double f = di / sub;
+        const double f = di * rcp_nr2(sub);
         dl[i] = f; dinv[i] = inv_pivot(sub); du[i] = dn; du2[i] = un;
         bits |= 1u << (i & 31);
         di = ui - f * dn;
@@ -704,7 +729,10 @@ __global__ void __launch_bounds__(32) inverse_iter_smem_kernel(const double* __r
     }
     if (p >= 2 && ((p - 2) & 31) != 31) sw[(p - 2) >> 5] = bits;
     dinv[p - 1] = inv_pivot(di);
-    for (int i = 0; i < p; ++i) bb[i] = 1.0 + 0.5 * sin(0.7 * (double)i + 0.3 * (double)j);
+    for (int i = 0; i < p; ++i) {  // deterministic start vector in [0.75, 1.25)
+      const unsigned h = ((unsigned)i * 2654435761u) ^ ((unsigned)(j + 1) * 2246822519u);
+      bb[i] = 0.75 + 0.5 * (double)((h >> 8) & 0xffffu) / 65536.0;
+    }
     double inv = 0.0;
     for (int rep = 0; rep < 2; ++rep) {
       if (rep == 1)
