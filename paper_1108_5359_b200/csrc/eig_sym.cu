@@ -991,8 +991,12 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
     err = cudaLaunchCooperativeKernel((void*)tridiag_kernel, grid, TT, args, tri_smem, st);
   }
   if (err != cudaSuccess) {
+    // not all blocks co-resident (an SM-limited context: MPS / green contexts): the caller takes
+    // its library path; anything else is an error
+    const bool too_large = err == cudaErrorCooperativeLaunchTooLarge;
+    (void)cudaGetLastError();
     set_error("eig_sym_above: tridiagonalisation launch failed: %s", cudaGetErrorString(err));
-    rc = L1F_ERR_CUDA;
+    rc = too_large ? L1F_ERR_UNSUPPORTED : L1F_ERR_CUDA;
   }
   if (rc == L1F_OK) {
     bounds_kernel<<<1, 256, 0, st>>>(d, e, e2, p, thr_abs, thr_rel, B);

@@ -284,7 +284,7 @@ static bool hand_eig(int p) {
 }
 
 static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double eta, double* out, int* rank,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool force_lib = false) {
   const bool right = n <= m;         // Gram of the smaller side
   const int p = (int)(right ? n : m), q = (int)(right ? m : n);
   // row-major W (m x n) == column-major X = W^T (n x m, ld n)
@@ -297,12 +297,13 @@ static int svt_gram(Handles* h, const double* W, int64_t m, int64_t n, double et
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)n, &zero, g.d(), p);
   else        // W W^T = X^T X
     cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)n, &zero, g.d(), p);
-  if (hand_eig(p)) {
+  if (!force_lib && hand_eig(p)) {
     // hand-written eigensolver (eig_sym.cu): only the eigenpairs with lambda > eta^2, descending
     Buf z(st);
     L1F_CUDA_TRY(z.alloc(sizeof(double) * (size_t)p * p));
     int kk = 0;
     int rc = l1f_eig_sym_above(g.d(), p, eta * eta, 0.0, ev.d(), z.d(), &kk, st);
+    if (rc == L1F_ERR_UNSUPPORTED) return svt_gram(h, W, m, n, eta, out, rank, st, true);
     if (rc) return rc;
     std::vector<double> lam((size_t)(kk > 0 ? kk : 1));
     if (kk > 0) L1F_CUDA_TRY(cudaMemcpyAsync(lam.data(), ev.p, sizeof(double) * (size_t)kk, cudaMemcpyDeviceToHost, st));
@@ -500,7 +501,7 @@ __global__ void eig_pack_kernel(const double* __restrict__ Z, const double* __re
 }
 
 static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t ldw, double* U, double* sig, double* V,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool force_lib = false) {
   const bool right = n <= m;
   const int p = (int)(right ? n : m), q = (int)(right ? m : n);
   Buf g(st), ev(st), work(st), info(st), inv(st);
@@ -513,13 +514,14 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
   if (right) cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, p, q, &one, W, (int)ldw, &zero, g.d(), p);
   else cublasDsyrk(h->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, p, q, &one, W, (int)ldw, &zero, g.d(), p);
   const int blocks = num_sms() * 4;
-  if (hand_eig(p)) {
+  if (!force_lib && hand_eig(p)) {
     // hand-written eigensolver: the triplets with sigma > 1e-7 sigma_max (every seed rank cut keeps
     // sigma > rank_tol * sigma_max with rank_tol >= 1e-6); the rest are returned as sigma = 0
     Buf z(st);
     L1F_CUDA_TRY(z.alloc(sizeof(double) * (size_t)p * p));
     int kk = 0;
     int rc = l1f_eig_sym_above(g.d(), p, 0.0, 1e-14, ev.d(), z.d(), &kk, st);
+    if (rc == L1F_ERR_UNSUPPORTED) return svd_gram(h, W, m, n, ldw, U, sig, V, st, true);
     if (rc) return rc;
     eig_pack_kernel<<<blocks, 256, 0, st>>>(z.d(), ev.d(), kk, p, right ? V : U, sig, inv.d());
     L1F_CHECK_LAUNCH();
@@ -589,7 +591,7 @@ extern "C" int l1f_init(void* stream) {
   cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, p, &one, a.d(), p, g.d(), p, &zero, z.d(), p);
   int k = 0;
   rc = l1f_eig_sym_above(g.d(), p, 0.0, 0.5, lam.d(), z.d(), &k, st);
-  if (rc) return rc;
+  if (rc && rc != L1F_ERR_UNSUPPORTED) return rc;  // (unsupported: the library path serves instead)
   L1F_CUDA_TRY(cudaStreamSynchronize(st));
   done = true;
   return L1F_OK;
