@@ -418,6 +418,8 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
                   "filters": t_filter_only, "filter_samples_ms": filter_samples, "factors": float(_med([e[2].elapsed_time(e[3]) for e in ev_all])),
                   "reconstruct": t_recon, "t1_seed_s": t1, "t1_first_call_s": t1_first, "generate_s": t_gen}
     traffic = ncu_traffic(cfgd)
+    fp64_filter = plan.filter_dtype == torch.float64
+    fp64_tflops = engine.fma_peak_tflops(fp64=True) if fp64_filter else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -426,12 +428,15 @@ def measure_config(cfgd, args, fma_tflops, e2e=True, cpu="full", local=0):
                    "r_prime": k, "tol": TOL, "parallelism": "1 GPU",
                    "filter_dtype": "f64" if plan.filter_dtype == torch.float64 else "f32",
                    "l2": "inputs larger than L2 (M is %.1f GB)" % (m * n * 4 / 1e9)},
-        "roofline": {"bound": "fp32", "kernel": ("adm_small_kernel, FP64 (column + row filters)"
-                                                   if plan.filter_dtype == torch.float64 else
-                                                   "adm_tc_kernel, tcgen05 bf16x3 (column + row filters)"), "achieved": achieved,
-                     "peak": fma_tflops, "unit": "TFLOP/s", "frac": achieved / fma_tflops,
-                     "peak_source": "measured FP32 FMA probe (l1f_fma_peak_probe, this run)",
-                     "peak_nominal": 148 * 128 * 2 * 1.965e9 / 1e12,
+        "roofline": ({"bound": "fp64", "kernel": "adm_small_kernel, FP64 (column + row filters)",
+                      "achieved": achieved, "peak": fp64_tflops, "unit": "TFLOP/s", "frac": achieved / fp64_tflops,
+                      "peak_source": "measured FP64 FMA probe (l1f_fma_peak_probe_f64, this run)",
+                      "peak_nominal": 148 * 64 * 2 * 1.965e9 / 1e12, "fp32_frac": achieved / fma_tflops}
+                     if fp64_filter else
+                     {"bound": "fp32", "kernel": "adm_tc_kernel, tcgen05 bf16x3 (column + row filters)",
+                      "achieved": achieved, "peak": fma_tflops, "unit": "TFLOP/s", "frac": achieved / fma_tflops,
+                      "peak_source": "measured FP32 FMA probe (l1f_fma_peak_probe, this run)",
+                      "peak_nominal": 148 * 128 * 2 * 1.965e9 / 1e12}) | {
                      "traffic": traffic.get("filter", {}).get("dram_bytes_per_launch"),
                      "traffic_source": traffic.get("filter", {}).get("source"),
                      "algorithmic_flops_per_step": flops, "kernel_ms_per_step": t_filter_only,

@@ -312,6 +312,8 @@ int l1f_pcp_f64(const double* M, int64_t m, int64_t n, double lam, double tol,
 /* FP32 FMA-throughput microbenchmark (roofline denominator for the filter kernel):
  * runs `iters` dependent-chain FMA loops on every SM; *flops_host = FLOPs executed. */
 int l1f_fma_peak_probe(int32_t iters, float* sink, double* flops_host, void* stream);
+/* the same for FP64 FMAs (sink: 8 x SMs doubles): the roofline of the FP64 small-k filter */
+int l1f_fma_peak_probe_f64(int32_t iters, double* sink, double* flops_host, void* stream);
 
 #ifdef __cplusplus
 }

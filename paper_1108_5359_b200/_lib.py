@@ -97,6 +97,7 @@ SIGNATURES = {
     "l1f_pcp_f64": (_int, [_vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp,
                            _vp, _vp, _vp, _vp]),
     "l1f_fma_peak_probe": (_int, [_i32, _vp, _vp, _vp]),
+    "l1f_fma_peak_probe_f64": (_int, [_i32, _vp, _vp, _vp]),
 }
 
 # library options (include/l1pcp_b200.h L1F_OPT_*): explicit process-wide switches of the kernel

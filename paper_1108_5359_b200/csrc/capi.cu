@@ -65,6 +65,21 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, float* sink) 
   if (s == 12345.678f) sink[blockIdx.x] = s;  // keeps the chains alive
 }
 
+__global__ void __launch_bounds__(256) fma_probe_f64_kernel(int iters, double* sink) {
+  double a0 = threadIdx.x * 1e-7, a1 = a0 + 1e-7, a2 = a0 + 2e-7, a3 = a0 + 3e-7;
+  double a4 = a0 + 4e-7, a5 = a0 + 5e-7, a6 = a0 + 6e-7, a7 = a0 + 7e-7;
+  const double b = 0.999999, c = 1e-9 * (blockIdx.x + 1);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+      a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) sink[blockIdx.x] = s;  // keeps the chains alive
+}
+
 }  // namespace l1f
 
 using namespace l1f;
@@ -97,6 +112,15 @@ extern "C" int l1f_fma_peak_probe(int32_t iters, float* sink, double* flops_host
   L1F_REQUIRE(iters > 0, L1F_ERR_ARG, "iters must be positive");
   const int blocks = num_sms() * 8;  // 8 x 256 threads = 64 warps per SM
   fma_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, sink);
+  L1F_CHECK_LAUNCH();
+  *flops_host = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+  return L1F_OK;
+}
+
+extern "C" int l1f_fma_peak_probe_f64(int32_t iters, double* sink, double* flops_host, void* stream) {
+  L1F_REQUIRE(iters > 0, L1F_ERR_ARG, "iters must be positive");
+  const int blocks = num_sms() * 8;
+  fma_probe_f64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, sink);
   L1F_CHECK_LAUNCH();
   *flops_host = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
   return L1F_OK;

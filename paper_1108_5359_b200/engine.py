@@ -601,16 +601,17 @@ def rel_err_device(a, b):
     return float(np.sqrt(d2) / np.sqrt(b2)) if b2 else float(np.sqrt(d2))
 
 
-def fma_peak_tflops(iters=4096, reps=3):
-    """Measured FP32 FMA throughput of this GPU (the filter kernel's roofline denominator)."""
-    sink = torch.zeros(_sm_count() * 8, dtype=torch.float32, device="cuda")
+def fma_peak_tflops(iters=4096, reps=3, fp64=False):
+    """Measured FP32 (or FP64) FMA throughput of this GPU (the filter kernels' roofline denominator)."""
+    sink = torch.zeros(_sm_count() * 8, dtype=torch.float64 if fp64 else torch.float32, device="cuda")
     flops = ctypes.c_double(0.0)
     best = 0.0
     for _ in range(reps + 1):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        _lib.call("l1f_fma_peak_probe", int(iters), dv.ptr(sink), ctypes.addressof(flops), dv.stream())
+        _lib.call("l1f_fma_peak_probe_f64" if fp64 else "l1f_fma_peak_probe", int(iters), dv.ptr(sink),
+                  ctypes.addressof(flops), dv.stream())
         b.record()
         b.synchronize()
         best = max(best, flops.value / (a.elapsed_time(b) * 1e-3) / 1e12)
