@@ -3,6 +3,7 @@ import sys, torch, numpy as np
 sys.path.insert(0, '.')
 import paper_1108_5359_b200 as l1pcp
 from paper_1108_5359_b200 import engine, _lib
+if len(sys.argv) > 3: _lib.load(sys.argv[3])
 from paper_1108_5359_b200.l1reg import filter_units
 from paper_1108_5359_b200.synth import BENCHMARK_CONFIGS
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 4
