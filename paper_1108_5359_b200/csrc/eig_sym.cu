@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(32) inverse_iter_smem_kernel(const double* __r
   for (int i = threadIdx.x; i < p; i += 32) y[i] = bb[i] * inv;
 }
 
-// back-transformation as backtransform_kernel: BT_VPB eigenvectors per block, each in shared memory
+// back-transformation as backtransform_kernel: BT_VPB eigenvectors per block, each in registers
 // and split over a group of BT_GW warps (thread t of the group owns columns t, t + 32 BT_GW, ...).
 // The reflector rows stream through shared memory in chunks of rc rows, double-buffered with
 // cp.async.  One pass per reflector applies it and forms the next reflector's dot with the updated
@@ -805,11 +805,14 @@ __global__ void __launch_bounds__(BT_T) backtransform_chunk_kernel(const double*
   if (j0 >= k) return;
   const int j = j0 + g;
   const bool live = j < k;
-  double* __restrict__ yv = bt_smem + (size_t)g * p;
-  double* chunks = bt_smem + (size_t)BT_VPB * p;  // 2 x rc rows of p
+  double* chunks = bt_smem;  // 2 x rc rows of p
   double* y = Y + (size_t)(live ? j : 0) * p;
-  if (live)
-    for (int c = t; c < p; c += BT_GT) yv[c] = y[c];
+  double yr[CM];  // this thread's columns t + BT_GT m of the vector, in registers
+#pragma unroll
+  for (int m = 0; m < CM; ++m) {
+    const int c = t + BT_GT * m;
+    yr[m] = (live && c < p) ? y[c] : 0.0;
+  }
   const int nrows = p - 1;  // reflectors 0 .. p-2, applied from p-2 down
   const int nch = (nrows + rc - 1) / rc;
   auto stage = [&](int ch) {
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(BT_T) backtransform_chunk_kernel(const double*
 #pragma unroll
       for (int m = 0; m < CM; ++m) {
         const int c = t + BT_GT * m;
-        const double x = (c > hi && c < p) ? vh[c] * yv[c] : 0.0;
+        const double x = (c > hi && c < p) ? vh[c] * yr[m] : 0.0;
         if (m & 1) a1 += x; else a0 += x;
       }
       double sr = gsum(a0 + a1) * __shfl_sync(0xffffffffu, tl, hi - lo);
@@ -864,10 +867,10 @@ __global__ void __launch_bounds__(BT_T) backtransform_chunk_kernel(const double*
           for (int m = 0; m < CM; ++m) {
             const int c = t + BT_GT * m;
             if (c >= r && c < p) {
-              double y0 = yv[c];
+              double y0 = yr[m];
               if (c > r) {
                 y0 = fma(-sr, vr[c], y0);
-                yv[c] = y0;
+                yr[m] = y0;
               }
               if (m & 1) b1 = fma(vn[c], y0, b1); else b0 = fma(vn[c], y0, b0);
             }
@@ -877,15 +880,20 @@ __global__ void __launch_bounds__(BT_T) backtransform_chunk_kernel(const double*
 #pragma unroll
           for (int m = 0; m < CM; ++m) {
             const int c = t + BT_GT * m;
-            if (c > r && c < p) yv[c] = fma(-sr, vr[c], yv[c]);
+            if (c > r && c < p) yr[m] = fma(-sr, vr[c], yr[m]);
           }
         }
       }
     }
     __syncthreads();  // buffer (ch & 1) is refilled by stage(ch + 2)
   }
-  if (live)
-    for (int c = t; c < p; c += BT_GT) y[c] = yv[c];
+  if (live) {
+#pragma unroll
+    for (int m = 0; m < CM; ++m) {
+      const int c = t + BT_GT * m;
+      if (c < p) y[c] = yr[m];
+    }
+  }
 }
 
 __global__ void symmetrize_kernel(double* __restrict__ A, int p) {
@@ -1025,10 +1033,11 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
           cudaFuncSetAttribute(cgs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * k));
           cgs2_kernel<<<1, 1024, sizeof(double) * (size_t)k, st>>>(Z, p, B, d, e, lam);
           rq_kernel<<<(k + 7) / 8, 256, 0, st>>>(Z, p, B, d, e, lam);
-          const size_t bt_vec = sizeof(double) * BT_VPB * (size_t)p;
-          const int bt_rc = bt_vec < 200 * 1024 ? (int)std::min<size_t>(32, (200 * 1024 - bt_vec) / (2 * sizeof(double) * p)) : 0;
+          // the vectors live in registers; the reflector chunks (double-buffered) in shared memory,
+          // sized for two blocks per SM
+          const int bt_rc = (int)std::min<size_t>(32, (100 * 1024) / (2 * sizeof(double) * p));
           if (bt_rc >= 2 && p <= 16 * BT_GT) {
-            const size_t bt_smem = bt_vec + 2 * sizeof(double) * (size_t)bt_rc * p;
+            const size_t bt_smem = 2 * sizeof(double) * (size_t)bt_rc * p;
             auto fn = p <= 4 * BT_GT ? backtransform_chunk_kernel<4>
                     : p <= 8 * BT_GT ? backtransform_chunk_kernel<8> : backtransform_chunk_kernel<16>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem);
