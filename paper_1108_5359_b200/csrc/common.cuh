@@ -72,6 +72,34 @@ __device__ __forceinline__ double tabs(double v) { return fabs(v); }
 __device__ __forceinline__ float  tmax(float a, float b)   { return fmaxf(a, b); }
 __device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
 
+// FP64 reciprocal and square root from the hardware estimates with Newton steps (within an ulp of
+// IEEE; off the division / sqrt subroutines, which cost ~10x more issue slots)
+__device__ __forceinline__ double rcp_nr2(double x) {
+  if (!(fabs(x) > 4.0 * DBL_MIN)) return 1.0 / x;  // the estimate flushes subnormals
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double sqrt_nr(double x) {  // x > 0 normal
+  if (!(x > 4.0 * DBL_MIN) || x > 1e300) return sqrt(x);
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  const double s = x * r;
+  return fma(0.5 * r, fma(-s, s, x), s);  // one correction of the root itself
+}
+// Householder reflector scalars of (alpha, x) with ||x||^2 = xnorm2 > 0 (LAPACK dlarfg without
+// the rescaling loop): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta,
+// v = x / (alpha - beta) (returned as its scale)
+__device__ __forceinline__ void householder_scalars(double alpha, double xnorm2, double& beta, double& tau,
+                                                    double& scale) {
+  beta = -copysign(sqrt_nr(fma(alpha, alpha, xnorm2)), alpha);
+  tau = (beta - alpha) * rcp_nr2(beta);
+  scale = rcp_nr2(alpha - beta);
+}
+
 // sign(w) * max(|w| - t, 0), the reference's soft threshold
 // (pkg/src/l1pcp/matcore.py:66-70; per-unit use at l1reg.py:97).
 template <typename T>

@@ -222,11 +222,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     for (int w = 0; w < DSM_W; ++w) xnorm2 += wsum[w];
     const double alpha = sc[0];
     double tau = 0.0, beta = alpha, scale = 0.0;
-    if (xnorm2 > 0.0) {
-      beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
+    if (xnorm2 > 0.0) householder_scalars(alpha, xnorm2, beta, tau, scale);
     double v[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
@@ -406,13 +402,7 @@ __device__ __forceinline__ int sturm_below_fast(const double* __restrict__ d, co
 
 // reciprocal from the hardware estimate and two Newton steps (within an ulp of 1 / x; off the
 // IEEE division's slow path, which dominates a dependent chain of p steps)
-__device__ __forceinline__ double rcp_nr2(double x) {
-  if (!(fabs(x) > 4.0 * DBL_MIN)) return 1.0 / x;  // the estimate flushes subnormals
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  r = r * fma(-x, r, 2.0);
-  return r * fma(-x, r, 2.0);
-}
+// rcp_nr2: common.cuh
 
 // count of eigenvalues below x with rcp_nr2 pivots (the threshold count of bounds_kernel)
 __device__ __forceinline__ int sturm_below_nr2(const double* __restrict__ d, const double* __restrict__ e2, int p,

@@ -385,95 +385,83 @@ __device__ __forceinline__ int sturm_count_below_fast(const double* __restrict__
 // v[c] = G[i][c] * hsc[i] for c > i + 1 (row i's tail is final once column i is reduced).
 __device__ void gram_tridiag(double* G, int ldg, int p, double* d, double* e, double* tau_s, double* hsc,
                              double* sy) {
-  // p <= kGramMaxP: each lane holds <= 4 entries of a row tail, each warp <= 4 trailing rows
-  constexpr int U = kGramMaxP / 32;
+  // per column: warp 0 forms the reflector; y = tau G v with one thread per trailing row (a full
+  // row dot, four accumulators: no shuffles); every warp forms K = -tau/2 y.v; the whole CTA
+  // applies the rank-2 update.  Three barriers per column.
+  __shared__ double scal[2];  // tau, scale
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+#ifdef L1F_SEED_PROF
+  long long tq[4] = {0, 0, 0, 0};
+  long long tp0 = clock64();
+#define TQ(k) do { if (threadIdx.x == 0) { long long _t = clock64(); tq[k] += _t - tp0; tp0 = _t; } } while (0)
+#else
+#define TQ(k) do {} while (0)
+#endif
   for (int i = 0; i + 1 < p; ++i) {
     const int c0 = i + 1;
     const double* gi = G + (int64_t)i * ldg;
-    double x[U];
-    double s = 0.0;
-#pragma unroll
-    for (int v = 0; v < U; ++v) {
-      const int c = c0 + lane + 32 * v;
-      x[v] = c < p ? gi[c] : 0.0;
-      if (c > c0) s = fma(x[v], x[v], s);
+    if (warp == 0) {
+      double s = 0.0;
+      for (int c = c0 + 1 + lane; c < p; c += 32) s = fma(gi[c], gi[c], s);
+      const double xnorm2 = warp_sum(s);
+      if (lane == 0) {
+        const double alpha = gi[c0];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (xnorm2 > 0.0) householder_scalars(alpha, xnorm2, beta, tau, scale);
+        d[i] = G[(int64_t)i * ldg + i];
+        e[i] = beta;
+        tau_s[i] = tau;
+        hsc[i] = scale;
+        scal[0] = tau;
+        scal[1] = scale;
+      }
     }
-    const double xnorm2 = warp_sum(s);  // the same value in every warp (same order)
-    const double alpha = gi[c0];
-    double tau = 0.0, beta = alpha, scale = 0.0;
-    if (xnorm2 > 0.0) {
-      beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-    if (threadIdx.x == 0) {
-      d[i] = G[(int64_t)i * ldg + i];
-      e[i] = beta;
-      tau_s[i] = tau;
-      hsc[i] = scale;
-    }
+    __syncthreads();
+    TQ(0);
+    const double tau = scal[0], scale = scal[1];
     if (tau == 0.0) continue;  // H = I (uniform)
-    double vv[U];
-#pragma unroll
-    for (int v = 0; v < U; ++v) vv[v] = (lane == 0 && v == 0) ? 1.0 : x[v] * scale;  // 0 beyond p
-    // y = tau G v over the trailing block: warp w takes rows c0 + w + 32 u
-    double a[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = c0 + warp + 32 * u;
-      a[u] = 0.0;
-      if (r < p) {
+    {
+      const int r = threadIdx.x;
+      if (r >= c0 && r < p) {
         const double* gr = G + (int64_t)r * ldg;
-#pragma unroll
-        for (int v = 0; v < U; ++v) {
-          const int c = c0 + lane + 32 * v;
-          if (c < p) a[u] = fma(gr[c], vv[v], a[u]);
+        double a0 = gr[c0], a1 = 0.0, a2 = 0.0, a3 = 0.0;  // v[c0] = 1
+        int c = c0 + 1;
+        for (; c + 3 < p; c += 4) {
+          a0 = fma(gr[c], gi[c] * scale, a0);
+          a1 = fma(gr[c + 1], gi[c + 1] * scale, a1);
+          a2 = fma(gr[c + 2], gi[c + 2] * scale, a2);
+          a3 = fma(gr[c + 3], gi[c + 3] * scale, a3);
         }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) a[u] += __shfl_xor_sync(0xffffffffu, a[u], o);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int r = c0 + warp + 32 * u;
-        if (r < p) sy[r] = tau * a[u];
+        for (; c < p; ++c) a0 = fma(gr[c], gi[c] * scale, a0);
+        sy[r] = tau * ((a0 + a1) + (a2 + a3));
       }
     }
     __syncthreads();
-    // w = y - (tau/2)(y.v) v ; G -= v w^T + w v^T (trailing block, both triangles)
-    double yc[U];
+    TQ(1);
+    // K = -tau/2 (y.v), every warp redundantly (same order: the same value everywhere)
     double dt = 0.0;
-#pragma unroll
-    for (int v = 0; v < U; ++v) {
-      const int c = c0 + lane + 32 * v;
-      yc[v] = c < p ? sy[c] : 0.0;
-      dt = fma(yc[v], vv[v], dt);
-    }
+    for (int c = c0 + lane; c < p; c += 32) dt = fma(sy[c], c == c0 ? 1.0 : gi[c] * scale, dt);
     const double K = -0.5 * tau * warp_sum(dt);
-    double wc[U];
-#pragma unroll
-    for (int v = 0; v < U; ++v) wc[v] = fma(K, vv[v], yc[v]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = c0 + warp + 32 * u;
-      if (r < p) {
-        const double vr = r == c0 ? 1.0 : gi[r] * scale;
-        const double wr = fma(K, vr, sy[r]);
-        double* gr = G + (int64_t)r * ldg;
-#pragma unroll
-        for (int v = 0; v < U; ++v) {
-          const int c = c0 + lane + 32 * v;
-          if (c < p) gr[c] -= fma(vr, wc[v], wr * vv[v]);
-        }
+    TQ(2);
+    // w = y - (tau/2)(y.v) v ; G -= v w^T + w v^T (trailing block, both triangles)
+    for (int r = c0 + warp; r < p; r += NW) {
+      const double vr = r == c0 ? 1.0 : gi[r] * scale;
+      const double wr = fma(K, vr, sy[r]);
+      double* gr = G + (int64_t)r * ldg;
+      for (int c = c0 + lane; c < p; c += 32) {
+        const double vc = c == c0 ? 1.0 : gi[c] * scale;
+        gr[c] -= fma(vr, fma(K, vc, sy[c]), wr * vc);
       }
     }
     __syncthreads();
+    TQ(3);
   }
+#ifdef L1F_SEED_PROF
+  if (threadIdx.x == 0 && p > 90 && blockIdx.x == 0)
+    printf("  tridiag p=%d per column: reflector %lld matvec %lld dot %lld update %lld\n", p, tq[0] / (p - 1),
+           tq[1] / (p - 1), tq[2] / (p - 1), tq[3] / (p - 1));
+#endif
+#undef TQ
   if (threadIdx.x == 0) d[p - 1] = G[(int64_t)(p - 1) * ldg + p - 1];
   __syncthreads();
 }
