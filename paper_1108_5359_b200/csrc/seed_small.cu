@@ -549,7 +549,7 @@ __device__ int tridiag_eig_above(const double* d, const double* e, double* e2, i
     const double clampv = eps * tnorm;
     auto inv_pivot = [clampv](double x) {
       if (fabs(x) < clampv) x = copysign(clampv, x == 0.0 ? 1.0 : x);
-      return 1.0 / x;
+      return rcp_nr2(x);
     };
     double di = d[0] - s, ui = p > 1 ? e[0] : 0.0;
     unsigned bits = 0;
@@ -559,12 +559,12 @@ __device__ int tridiag_eig_above(const double* d, const double* e, double* e2, i
       const double un = i + 2 < p ? e[i + 1] : 0.0;
       const size_t o = (size_t)i * ld;
       if (fabs(di) >= fabs(sub)) {
-        const double f = di != 0.0 ? sub / di : 0.0;
+        const double f = di != 0.0 ? sub * rcp_nr2(di) : 0.0;
         dl[o] = f; dinv[o] = inv_pivot(di); du[o] = ui; du2[o] = 0.0;
         di = dn - f * ui;
         ui = un;
       } else {
-        const double f = di / sub;
+        const double f = di * rcp_nr2(sub);
         dl[o] = f; dinv[o] = inv_pivot(sub); du[o] = dn; du2[o] = un;
         bits |= 1u << (i & 31);
         di = ui - f * dn;
