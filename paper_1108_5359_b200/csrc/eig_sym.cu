@@ -177,25 +177,26 @@ constexpr int DSM_W = DSM_T / 32;
 constexpr int DSM_R = 16;  // rows per block at most
 
 // ybuf, rowbuf: p x p slots (column i's y; row r's published values); part: p x G slots
-template <int CPT>
-__global__ void __launch_bounds__(DSM_T, 1)
+template <int CPT, int NTH>
+__global__ void __launch_bounds__(NTH, 1)
 tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, double* __restrict__ e,
                    double* __restrict__ tau_out, double* __restrict__ Vh, double* ybuf, double* part, double* rowbuf,
                    unsigned* cnt) {
+  constexpr int NWP = NTH / 32;
   extern __shared__ double As[];  // R x p, row q = global row b + q G
-  __shared__ double red[DSM_W][DSM_R + 1];
-  __shared__ double wsum[DSM_W];
+  __shared__ double red[NWP][DSM_R + 1];
+  __shared__ double wsum[NWP];
   __shared__ double vq[DSM_R], yq[DSM_R];
   __shared__ double sc[4];
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int R = b < p ? (p - 1 - b) / G + 1 : 0;
   for (int q = 0; q < R; ++q)
-    for (int c = tid; c < p; c += DSM_T) As[(size_t)q * p + c] = A[(size_t)(b + q * G) * p + c];
+    for (int c = tid; c < p; c += NTH) As[(size_t)q * p + c] = A[(size_t)(b + q * G) * p + c];
   double cur[CPT];
   int ownq[CPT];  // this thread's columns that are rows of this block: their index q, else -1
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
-    const int c = tid + DSM_T * j;
+    const int c = tid + NTH * j;
     cur[j] = c < p ? A[c] : 0.0;
     ownq[j] = (c < p && c >= b && (c - b) % G == 0) ? (c - b) / G : -1;
   }
@@ -210,7 +211,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-      const int c = tid + DSM_T * j;
+      const int c = tid + NTH * j;
       if (c > c0 && c < p) s = fma(cur[j], cur[j], s);
       if (c == c0) sc[0] = cur[j];
       if (c == i && b == 0) d[i] = cur[j];
@@ -219,14 +220,14 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     if (lane == 0) wsum[warp] = s;
     __syncthreads();
     double xnorm2 = 0.0;
-    for (int w = 0; w < DSM_W; ++w) xnorm2 += wsum[w];
+    for (int w = 0; w < NWP; ++w) xnorm2 += wsum[w];
     const double alpha = sc[0];
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (xnorm2 > 0.0) householder_scalars(alpha, xnorm2, beta, tau, scale);
     double v[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-      const int c = tid + DSM_T * j;
+      const int c = tid + NTH * j;
       v[j] = c == c0 ? 1.0 : ((c > c0 && c < p) ? cur[j] * scale : 0.0);
       if (c >= c0 && c < p) {
         if (b == 0) Vh[(size_t)i * p + c] = v[j];
@@ -247,7 +248,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
         const double* ar = As + (size_t)q * p;
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
-          const int c = tid + DSM_T * j;
+          const int c = tid + NTH * j;
           if (c < p) acc[q] = fma(ar[c], v[j], acc[q]);
         }
       }
@@ -277,7 +278,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
         const int r = b + lane * G;
         double t = 0.0;
         if (lane < R && r >= c0) {
-          for (int w = 0; w < DSM_W; ++w) t += red[w][lane];
+          for (int w = 0; w < NWP; ++w) t += red[w][lane];
           t *= tau;
           ycol[r] = t;
           pv = t * vq[lane];
@@ -311,7 +312,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     double yv[CPT], nx[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-      const int c = tid + DSM_T * j;
+      const int c = tid + NTH * j;
       const bool live = c >= c0 && c < p;
       yv[j] = live ? __ldcg(ycol + c) : 0.0;
       nx[j] = live ? (i == 0 ? A[(size_t)p + c] : __ldcg(rowbuf + (size_t)c0 * p + c)) : 0.0;
@@ -332,13 +333,13 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
       double* ar = As + (size_t)q * p;
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
-        const int c = tid + DSM_T * j;
+        const int c = tid + NTH * j;
         if (c >= c0 && c < p) ar[c] -= fma(vr, w[j], wr * v[j]);
       }
     }
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-      const int c = tid + DSM_T * j;
+      const int c = tid + NTH * j;
       cur[j] = (c >= c0 && c < p) ? nx[j] - fma(1.0, w[j], wc0 * v[j]) : 0.0;
     }
     // ---- publish row i + 2 (current through column i) for the copies at column i + 1
@@ -347,7 +348,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
       const double* ar = As + (size_t)(r2 / G) * p;
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
-        const int c = tid + DSM_T * j;
+        const int c = tid + NTH * j;
         if (c >= r2 && c < p) rowbuf[(size_t)r2 * p + c] = ar[c];
       }
     }
@@ -362,7 +363,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
   if (b == 0) {
 #pragma unroll
     for (int j = 0; j < CPT; ++j)
-      if (tid + DSM_T * j == p - 1) d[p - 1] = cur[j];
+      if (tid + NTH * j == p - 1) d[p - 1] = cur[j];
   }
 }
 
@@ -911,7 +912,7 @@ bool l1f_eig_dsm_applies(int p) {
   if (nsm <= 0 || nsm > 256 || p < 2) return false;
   const int rmax = (p + nsm - 1) / nsm;
   const size_t dsm_static = sizeof(double) * (DSM_W * (DSM_R + 1) + DSM_W + 2 * DSM_R + 4) + 64;
-  return rmax <= DSM_R && p <= 8 * DSM_T && sizeof(double) * (size_t)rmax * p + dsm_static <= (size_t)optin;
+  return rmax <= DSM_R && p <= 2048 && sizeof(double) * (size_t)rmax * p + dsm_static <= (size_t)optin;
 }
 
 // Eigenpairs of the symmetric p x p matrix G (column-major lower triangle as cuBLAS syrk leaves it,
@@ -980,10 +981,13 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
     L1F_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)p, st));
     const double* Ac = G;
     void* dargs[] = {(void*)&Ac, &p, &d, &e, &tau, &Vh, &ybuf, &dpart, &rowbuf, &cnt};
-    void* fn = p <= 2 * DSM_T ? (void*)tridiag_dsm_kernel<2>
-               : p <= 4 * DSM_T ? (void*)tridiag_dsm_kernel<4> : (void*)tridiag_dsm_kernel<8>;
+    // 256 threads per block up to p = 1024, 512 beyond (measured, tools/r2/dsm_threads_ab.py: 128
+    // threads cost cfg3 +12 %; 512 threads cfg2 +8 %, cfg3 even, cfg5 -5 %)
+    const int nth = p > 1024 ? 512 : DSM_T;
+    void* fn = nth == 512 ? (void*)tridiag_dsm_kernel<4, 512>
+               : p <= 2 * DSM_T ? (void*)tridiag_dsm_kernel<2, DSM_T> : (void*)tridiag_dsm_kernel<4, DSM_T>;
     L1F_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_smem));
-    err = cudaLaunchCooperativeKernel(fn, nsm, DSM_T, dargs, dsm_smem, st);
+    err = cudaLaunchCooperativeKernel(fn, nsm, nth, dargs, dsm_smem, st);
   } else {
     void* args[] = {&G, &p, &d, &e, &tau, &Vh, &pv, &part};
     err = cudaLaunchCooperativeKernel((void*)tridiag_kernel, grid, TT, args, tri_smem, st);
