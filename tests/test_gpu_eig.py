@@ -53,12 +53,14 @@ def _pcp_case(m, n, r, seed, rho=0.1):
     return torch.from_numpy(low + sp).cuda()
 
 
-@pytest.mark.parametrize("m,n,r", [(130, 120, 6), (120, 300, 8), (400, 160, 12), (700, 600, 30)])
-@pytest.mark.parametrize("dsm", [1, 0])
+@pytest.mark.parametrize("m,n,r,dsm", [(130, 120, 6, 1), (120, 300, 8, 1), (400, 160, 12, 1), (700, 600, 30, 1),
+                                       (130, 120, 6, 0), (120, 300, 8, 0), (400, 160, 12, 0), (700, 600, 30, 0),
+                                       (1500, 1300, 40, 1)])
 def test_large_block_pcp_matches_syevd(m, n, r, dsm):
     """The ALM loop on blocks beyond the one-CTA kernel with the hand-written eigensolver (shared-
     memory-resident or L2-resident tridiagonalisation; p = min(m, n) from 120, fewer rows than the
-    148 blocks, to 600) against the syevd path: same iterations and rank, L to 1e-12."""
+    148 blocks, to 1300, where the 512-thread form runs) against the syevd path: same iterations and
+    rank, L to 1e-12."""
     from paper_1108_5359_b200 import pcp_adm
     M = _pcp_case(m, n, r, m * 7 + n)
     cfg = pcp_adm.AdmConfig(tol=1e-7)
