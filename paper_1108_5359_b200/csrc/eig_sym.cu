@@ -911,7 +911,8 @@ bool l1f_eig_dsm_applies(int p) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (nsm <= 0 || nsm > 256 || p < 2) return false;
   const int rmax = (p + nsm - 1) / nsm;
-  const size_t dsm_static = sizeof(double) * (DSM_W * (DSM_R + 1) + DSM_W + 2 * DSM_R + 4) + 64;
+  const int nw = p > 1024 ? 16 : DSM_W;  // warps of the variant that runs (512 / 256 threads)
+  const size_t dsm_static = sizeof(double) * (nw * (DSM_R + 1) + nw + 2 * DSM_R + 4) + 64;
   return rmax <= DSM_R && p <= 2048 && sizeof(double) * (size_t)rmax * p + dsm_static <= (size_t)optin;
 }
 
