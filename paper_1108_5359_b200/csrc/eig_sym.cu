@@ -177,7 +177,7 @@ constexpr int DSM_W = DSM_T / 32;
 constexpr int DSM_R = 16;  // rows per block at most
 
 // ybuf, rowbuf: p x p slots (column i's y; row r's published values); part: p x G slots
-template <int CPT, int NTH>
+template <int CPT, int NTH, int RM>  // RM: rows per block at most (8 or 16)
 __global__ void __launch_bounds__(NTH, 1)
 tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, double* __restrict__ e,
                    double* __restrict__ tau_out, double* __restrict__ Vh, double* ybuf, double* part, double* rowbuf,
@@ -219,8 +219,7 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     s = warp_sum(s);
     if (lane == 0) wsum[warp] = s;
     __syncthreads();
-    double xnorm2 = 0.0;
-    for (int w = 0; w < NWP; ++w) xnorm2 += wsum[w];
+    const double xnorm2 = warp_sum(lane < NWP ? wsum[lane] : 0.0);  // same tree in every warp
     const double alpha = sc[0];
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (xnorm2 > 0.0) householder_scalars(alpha, xnorm2, beta, tau, scale);
@@ -240,9 +239,9 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
     }
     EPROF(0);
     // ---- y = tau A v over this block's rows r >= c0
-    double acc[DSM_R];
+    double acc[RM];
 #pragma unroll
-    for (int q = 0; q < DSM_R; ++q) {
+    for (int q = 0; q < RM; ++q) {
       acc[q] = 0.0;
       if (q < R && b + q * G >= c0) {
         const double* ar = As + (size_t)q * p;
@@ -253,10 +252,10 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
         }
       }
     }
-    // transpose-reduce: 16 values per lane -> lane pairs holding one row's warp sum
+    // transpose-reduce: RM values per lane -> lane groups holding one row's warp sum
 #pragma unroll
-    for (int h = 8; h >= 1; h >>= 1) {
-      const int o = h * 2;  // lane distance 16, 8, 4, 2
+    for (int h = RM / 2; h >= 1; h >>= 1) {
+      const int o = h * (32 / RM);  // lane distance 16, 8, ... (RM = 16: 16, 8, 4, 2; RM = 8: 16, 8, 4)
       const bool upper = (lane & o) != 0;
 #pragma unroll
       for (int q = 0; q < h; ++q) {
@@ -265,16 +264,19 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
         acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-    const int qrow = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    if ((lane & 1) == 0) red[warp][qrow] = acc[0];
+#pragma unroll
+    for (int o = 32 / RM / 2; o >= 1; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+    int qrow = 0;
+#pragma unroll
+    for (int h = RM / 2, o = 16; h >= 1; h >>= 1, o >>= 1) qrow += (lane & o) ? h : 0;
+    if ((lane & (32 / RM - 1)) == 0) red[warp][qrow] = acc[0];
     __syncthreads();
     double* ycol = ybuf + (size_t)i * p;
     double* pcol = part + (size_t)i * G;
     EPROF(1);
     if (warp == 0) {
       double pv = 0.0;
-      if (lane < DSM_R) {
+      if (lane < RM) {
         const int r = b + lane * G;
         double t = 0.0;
         if (lane < R && r >= c0) {
@@ -985,8 +987,9 @@ int l1f_eig_sym_above(double* G, int p, double thr_abs, double thr_rel, double* 
     // 256 threads per block up to p = 1024, 512 beyond (measured, tools/r2/dsm_threads_ab.py: 128
     // threads cost cfg3 +12 %; 512 threads cfg2 +8 %, cfg3 even, cfg5 -5 %)
     const int nth = p > 1024 ? 512 : DSM_T;
-    void* fn = nth == 512 ? (void*)tridiag_dsm_kernel<4, 512>
-               : p <= 2 * DSM_T ? (void*)tridiag_dsm_kernel<2, DSM_T> : (void*)tridiag_dsm_kernel<4, DSM_T>;
+    void* fn = nth == 512 ? (rmax <= 8 ? (void*)tridiag_dsm_kernel<4, 512, 8> : (void*)tridiag_dsm_kernel<4, 512, 16>)
+               : p <= 2 * DSM_T ? (rmax <= 8 ? (void*)tridiag_dsm_kernel<2, DSM_T, 8> : (void*)tridiag_dsm_kernel<2, DSM_T, 16>)
+                                : (rmax <= 8 ? (void*)tridiag_dsm_kernel<4, DSM_T, 8> : (void*)tridiag_dsm_kernel<4, DSM_T, 16>);
     L1F_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_smem));
     err = cudaLaunchCooperativeKernel(fn, nsm, nth, dargs, dsm_smem, st);
   } else {
