@@ -389,6 +389,7 @@ __device__ void gram_tridiag(double* G, int ldg, int p, double* d, double* e, do
   // row dot, four accumulators: no shuffles); every warp forms K = -tau/2 y.v; the whole CTA
   // applies the rank-2 update.  Three barriers per column.
   __shared__ double scal[2];  // tau, scale
+  __shared__ double dtp[kGramMaxP / 32];  // per-warp partials of y.v
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
 #ifdef L1F_SEED_PROF
   long long tq[4] = {0, 0, 0, 0};
@@ -420,8 +421,9 @@ __device__ void gram_tridiag(double* G, int ldg, int p, double* d, double* e, do
     TQ(0);
     const double tau = scal[0], scale = scal[1];
     if (tau == 0.0) continue;  // H = I (uniform)
-    {
+    if (warp < kGramMaxP / 32) {  // rows live in threads 0 .. p - 1 (p <= 128: warps 0 - 3)
       const int r = threadIdx.x;
+      double yv = 0.0;
       if (r >= c0 && r < p) {
         const double* gr = G + (int64_t)r * ldg;
         double a0 = gr[c0], a1 = 0.0, a2 = 0.0, a3 = 0.0;  // v[c0] = 1
@@ -433,15 +435,17 @@ __device__ void gram_tridiag(double* G, int ldg, int p, double* d, double* e, do
           a3 = fma(gr[c + 3], gi[c + 3] * scale, a3);
         }
         for (; c < p; ++c) a0 = fma(gr[c], gi[c] * scale, a0);
-        sy[r] = tau * ((a0 + a1) + (a2 + a3));
+        const double y = tau * ((a0 + a1) + (a2 + a3));
+        sy[r] = y;
+        yv = y * (r == c0 ? 1.0 : gi[r] * scale);  // y_r v_r: this row's share of y.v
       }
+      yv = warp_sum(yv);
+      if (lane == 0) dtp[warp] = yv;
     }
     __syncthreads();
     TQ(1);
-    // K = -tau/2 (y.v), every warp redundantly (same order: the same value everywhere)
-    double dt = 0.0;
-    for (int c = c0 + lane; c < p; c += 32) dt = fma(sy[c], c == c0 ? 1.0 : gi[c] * scale, dt);
-    const double K = -0.5 * tau * warp_sum(dt);
+    // K = -tau/2 (y.v) from the four row warps' partials (fixed order)
+    const double K = -0.5 * tau * ((dtp[0] + dtp[1]) + (dtp[2] + dtp[3]));
     TQ(2);
     // w = y - (tau/2)(y.v) v ; G -= v w^T + w v^T (trailing block, both triangles)
     for (int r = c0 + warp; r < p; r += NW) {
