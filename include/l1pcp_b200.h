@@ -84,8 +84,8 @@ int l1f_get_option(int key, int64_t* value_host);
 const char* l1f_last_error(void);
 int l1f_version(void);
 /* one-time initialisation on the current device (the cuBLAS handle and its first GEMMs, the
- * eigensolver's kernels); idempotent per host thread.  The Python layer calls it once after loading
- * the library; a caller that skips it pays the same cost inside its first seed solve. */
+ * eigensolver's kernels); idempotent per device and host thread.  The Python layer calls it once
+ * after loading the library; a caller that skips it pays the same cost inside its first seed solve. */
 int l1f_init(void* stream);
 /* number of SMs of the current device, written to *out_host */
 int l1f_sm_count(int* out_host);

@@ -47,7 +47,11 @@ struct Handles {
 // cuBLAS on every call; the cuSOLVER handle only when a cuSOLVER routine runs (its creation loads
 // the library's modules, ~0.1 s, which the default seed path never needs)
 static int handles(cudaStream_t st, Handles*& out) {
-  static thread_local Handles h;
+  // one set per device (a cuBLAS / cuSOLVER handle belongs to the device current at its creation)
+  static thread_local Handles hs[64];
+  int dev = 0;
+  L1F_CUDA_TRY(cudaGetDevice(&dev));
+  Handles& h = hs[dev & 63];
   if (!h.blas) {
     if (cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS) {
       set_error("cublasCreate failed");
@@ -569,7 +573,10 @@ static int svd_gram(Handles* h, const double* W, int64_t m, int64_t n, int64_t l
 // and its first dsyrk / dgemm (cuBLAS loads its kernels on first use), and one small run of the
 // hand-written eigensolver so its kernels are loaded; idempotent per host thread
 extern "C" int l1f_init(void* stream) {
-  static thread_local bool done = false;
+  static thread_local bool done_dev[64] = {};
+  int dev = 0;
+  L1F_CUDA_TRY(cudaGetDevice(&dev));
+  bool& done = done_dev[dev & 63];
   if (done) return L1F_OK;
   cudaStream_t st = (cudaStream_t)stream;
   Handles* h;
