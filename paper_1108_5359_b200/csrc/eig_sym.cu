@@ -369,21 +369,6 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
   }
 }
 
-// number of eigenvalues of T (d, e2 = e^2) below x
-__device__ __forceinline__ int sturm_below(const double* __restrict__ d, const double* __restrict__ e2, int p, double x,
-                                           double pivmin) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  cnt += q < 0.0;
-  for (int j = 1; j < p; ++j) {
-    q = (d[j] - x) - e2[j - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
-  }
-  return cnt;
-}
-
 // the same count with the hardware reciprocal estimate and one Newton step in place of the division
 // (relative error ~2^-46 per pivot, far below the multisection's resolution); bisection only
 __device__ __forceinline__ int sturm_below_fast(const double* __restrict__ d, const double* __restrict__ e2, int p,
