@@ -369,8 +369,8 @@ tridiag_dsm_kernel(const double* __restrict__ A, int p, double* __restrict__ d, 
   }
 }
 
-// the same count with the hardware reciprocal estimate and one Newton step in place of the division
-// (relative error ~2^-46 per pivot, far below the multisection's resolution); bisection only
+// number of eigenvalues of T (d, e2 = e^2) below x (Sturm count), with the hardware reciprocal
+// estimate and one Newton step per pivot (relative error ~2^-46, far below the multisection's resolution)
 __device__ __forceinline__ int sturm_below_fast(const double* __restrict__ d, const double* __restrict__ e2, int p,
                                                 double x, double pivmin) {
   int cnt = 0;
