@@ -1,17 +1,18 @@
 // Eigenpairs of a symmetric matrix above a threshold, hand-written (the Gram step of the large-seed
 // SVT, seed.cu svt_gram / svd_gram; reference: the SVD inside svt_with_rank, matcore.py:73-105).
 //
-//   1. Householder tridiagonalisation T = Q^T G Q (LAPACK dsytd2 'L' order), one cooperative kernel:
-//      per column two grid-wide barriers (p = tau A v with partial dot products; then the rank-2
-//      update A -= v w^T + w v^T of the trailing block); the full symmetric matrix is kept so rows
-//      are contiguous; every block recomputes the reflector redundantly (no extra barrier).
+//   1. Householder tridiagonalisation T = Q^T G Q (LAPACK dsytd2 'L' order).  Default
+//      (tridiag_dsm_kernel, p <= 2000): G resident in the shared memory of all SMs, rows owned per
+//      block, one counter barrier per column (see the kernel).  Otherwise (tridiag_kernel): G in
+//      L2, two grid-wide barriers per column.
 //   2. The k eigenvalues of T above the threshold: a Sturm count gives k, each eigenvalue is
 //      bracketed by multisection (one warp per eigenvalue, 32 Sturm counts per round).
 //   3. Eigenvectors of T by inverse iteration (tridiagonal LU with partial pivoting, two solves per
-//      eigenvalue, one thread each), then modified Gram-Schmidt over the k vectors in descending
-//      order (nearly equal shifts of a cluster give nearly parallel vectors: MGS keeps the cluster's
-//      span) and Rayleigh quotients as the final eigenvalues.
-//   4. Back-transformation Z = Q Y, one warp per eigenvector (reflectors applied in reverse order).
+//      eigenvalue; one block per eigenvalue with its factors in shared memory), then classical
+//      Gram-Schmidt twice inside clusters of nearly equal eigenvalues, normalisation and Rayleigh
+//      quotients as the final eigenvalues (one warp per vector).
+//   4. Back-transformation Z = Q Y: each vector split over a group of warps and held in
+//      registers, the reflector rows streamed through shared memory (cp.async, double-buffered).
 // No library call; the host reads k and the eigenvalues once.
 #include "common.cuh"
 
